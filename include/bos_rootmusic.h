@@ -1,0 +1,155 @@
+/*
+ * bos_rootmusic.h — C ABI of libbosrm.so: B200 (sm_100a) windowed root-MUSIC fringe
+ * demodulation for DOE-based background oriented schlieren (arxiv 1910.11872).
+ *
+ * No CUDA or torch types appear in these signatures: pointers are plain addresses
+ * (device or host as stated per argument), sizes are ints, streams are `void*`
+ * (a cudaStream_t; NULL = the legacy default stream).
+ *
+ * Citations: P:L<n> = line of the paper's LaTeX source; Eq.(n) = the paper's
+ * equation n; [Rn] = reading of a silent/ambiguous passage, listed in DESIGN.md §3.
+ *
+ * ----------------------------------------------------------------------------------
+ * What one call computes (Algorithm 1, for every pixel of every frame):
+ *   Γ_w    = M×M window of the complex fringe signal around (px,py)      Eq.(2)
+ *            rows ↔ y, columns ↔ x [R4]; offsets o = -⌊(M-1)/2⌋..⌊M/2⌋ [R2];
+ *            out-of-frame samples clamp to the nearest edge sample [R1]
+ *   R_y    = Γ_w Γ_w^H (sample autocorrelation, no averaging)            Eq.(4)
+ *   u_1    = dominant eigenvector of R_y; v_1 ∝ Γ_w^H u_1 (SVD identity)  P:L206, Eqs.(7)-(11)
+ *   U_nU_n^H = I - u_1u_1^H,  V_nV_n^H = I - v_1v_1^H                    Eqs.(11),(14)
+ *   P_y(z) = z^{M-1} u_1^H(z) U_nU_n^H u_1(z), P_x likewise (degree 2M-2) Eqs.(12),(13)
+ *   z_y,z_x= root closest to the unit circle (inside, tolerance band)    P:L207-208 [R6]
+ *   α      = ∠ Σ Γ_w e^{-j(ω_x x + ω_y y)},  ω_y = arg z_y, ω_x = -arg z_x Eq.(15)
+ *   out    = wrap(α - ref_phase) into (-π, π]  (raw α if ref_phase == NULL) [R7]
+ * ----------------------------------------------------------------------------------
+ *
+ * Error convention: every entry point returns an int status (BOS_OK or a negative
+ * code) and never aborts or exits.  Asynchronous device faults surface at the caller's
+ * next synchronisation (CUDA semantics).  bos_strerror() maps a code to a static string.
+ * The library keeps no global mutable state: calls are re-entrant and thread-safe across
+ * streams.
+ */
+#ifndef BOS_ROOTMUSIC_H
+#define BOS_ROOTMUSIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* complex64, interleaved (re, im) — the layout of Γ(x,y,t), Eq.(1) */
+typedef struct { float re, im; } bos_cf32;
+
+enum {
+    BOS_OK = 0,
+    BOS_ERR_INVALID_ARG = -1,   /* NULL required pointer, bad size, aliasing, host/device mix-up */
+    BOS_ERR_UNSUPPORTED = -2,   /* model_order != 3, or window_len outside the instantiated range */
+    BOS_ERR_CUDA = -3           /* a CUDA runtime call or kernel launch failed */
+};
+
+/* Per-pixel status bits written to `flags` (DESIGN.md §3 [R8]; the paper has no failure
+ * handling).  Flagged pixels still receive the computed value. */
+enum {
+    BOS_FLAG_NONCONVERGED = 1 << 0,  /* eigen/root iteration cap hit, or no finite root */
+    BOS_FLAG_AMBIGUOUS = 1 << 1,     /* two distinct-frequency root pairs within 1e-3 in |ln|z|| */
+    BOS_FLAG_SMALL_GAP = 1 << 2,     /* (oracle only) σ1²/σ2² < 1.3 */
+    BOS_FLAG_LOW_AMPLITUDE = 1 << 3, /* |Σ Γ_w e^{-j(...)}| < 1e-4 · M · ‖Γ_w‖_F */
+    BOS_FLAG_NONFINITE = 1 << 4,     /* window has NaN/Inf; output is NaN */
+    BOS_FLAG_BORDER = 1 << 5         /* informational: window clamped at the frame edge */
+};
+
+/* Window sizes with an instantiated kernel (window_len = M = 2L+1 in the paper, P:L98,
+ * P:L130; even M allowed [R2]). */
+#define BOS_WINDOW_LEN_MIN 3
+#define BOS_WINDOW_LEN_MAX 16
+#define BOS_MODEL_ORDER 3   /* Eq.(3): φ_w = α + ω_x x + ω_y y, three parameters [R3] */
+
+/*
+ * bos_rootmusic_demod — demodulate n_frames frames (Algorithm 1 over every pixel).
+ *
+ *   frames      DEVICE, [n_frames][H][W] bos_cf32, row-major, y slow; read only.
+ *               Γ(x,y,t) of Eq.(1): the analytic (complex) fringe signal, carrier allowed.
+ *   n_frames    ≥ 1.   H, W: frame height/width in pixels, each ≥ window_len (SPEC's
+ *               FieldTooSmall).  All device offsets are 64-bit (n_frames·H·W may exceed 2^31).
+ *   window_len  M, the window side = covariance order, in
+ *               [BOS_WINDOW_LEN_MIN, BOS_WINDOW_LEN_MAX].
+ *   model_order must be BOS_MODEL_ORDER (3), else BOS_ERR_UNSUPPORTED.
+ *   ref_phase   DEVICE [H][W] float32 wrapped reference phase, or NULL → out = raw α.
+ *               May alias a frame-slice of an earlier out_phase; must not alias out_phase.
+ *   out_phase   DEVICE [n_frames][H][W] float32, wrapped into (-π, π]; written.
+ *               Must not overlap `frames`.
+ *   flags       DEVICE [n_frames][H][W] uint8 status bits, or NULL (not written).
+ *   stream      cudaStream_t (NULL = legacy default stream).  Asynchronous: returns after
+ *               the launch; results are valid once `stream` has been synchronised.
+ * Ownership: the caller owns and allocates every buffer; the library allocates nothing.
+ * Determinism: no atomics on outputs; bitwise identical across runs and frame shardings.
+ */
+int bos_rootmusic_demod(const bos_cf32* frames, int n_frames, int H, int W,
+                        int window_len, int model_order, const float* ref_phase,
+                        float* out_phase, uint8_t* flags, void* stream);
+
+/*
+ * bos_rootmusic_demod_stack — a time-lapse stack against its own reference frame
+ * (BASELINE north_star: "each flow frame's phase is differenced against the reference
+ * frame").  Two stream-ordered launches:
+ *   ref_phase_out ← raw α of frames[ref_index];  out[t] ← wrap(α_t − ref_phase_out).
+ *   ref_index      0 ≤ ref_index < n_frames.
+ *   ref_phase_out  DEVICE [H][W] float32, written (caller-owned scratch / result).
+ * Other arguments as bos_rootmusic_demod.  out[ref_index] is exactly 0 where finite.
+ */
+int bos_rootmusic_demod_stack(const bos_cf32* frames, int n_frames, int H, int W,
+                              int window_len, int model_order, int ref_index,
+                              float* ref_phase_out, float* out_phase, uint8_t* flags,
+                              void* stream);
+
+/*
+ * bos_rootmusic_host_workspace_bytes — DEVICE scratch size needed by
+ * bos_rootmusic_demod_stack_host for frames of H×W processed chunk_frames at a time
+ * (two ping-pong slots of frames + outputs + flags, plus the reference phase).
+ * Returns 0 on invalid arguments.
+ */
+size_t bos_rootmusic_host_workspace_bytes(int H, int W, int chunk_frames, int with_flags);
+
+/*
+ * bos_rootmusic_demod_stack_host — bos_rootmusic_demod_stack on HOST buffers: the frames
+ * are streamed host→device in chunks of chunk_frames, demodulated, and the phases (and
+ * flags) streamed back, with the copies of one chunk overlapping the kernels of the
+ * other on two internal streams (created and destroyed inside the call).
+ *   h_frames     HOST [n_frames][H][W] bos_cf32 (pinned for full overlap; pageable works).
+ *   h_out_phase  HOST [n_frames][H][W] float32, written.  h_flags: HOST uint8 or NULL.
+ *   d_workspace  DEVICE scratch of ≥ bos_rootmusic_host_workspace_bytes(H, W, chunk_frames,
+ *                h_flags != NULL) bytes, caller-owned.
+ *   stream       the caller's stream; all work is ordered after prior work on it, and the
+ *                host buffers are valid once `stream` is synchronised.
+ */
+int bos_rootmusic_demod_stack_host(const bos_cf32* h_frames, int n_frames, int H, int W,
+                                   int window_len, int model_order, int ref_index,
+                                   float* h_out_phase, uint8_t* h_flags,
+                                   void* d_workspace, size_t workspace_bytes,
+                                   int chunk_frames, void* stream);
+
+/*
+ * bos_rootmusic_iteration_counts — measurement support for the roofline:
+ * runs the same kernel with per-pixel iteration counters over `frames` (DEVICE, as in
+ * bos_rootmusic_demod) and accumulates into d_counters (DEVICE, 4 × uint64, caller zeroes):
+ *   [0] pixels processed, [1] Σ power iterations, [2] Σ Aberth sweeps (y), [3] Σ Aberth
+ * sweeps (x).  Results identical to bos_rootmusic_demod (out_phase is written too).
+ */
+int bos_rootmusic_iteration_counts(const bos_cf32* frames, int n_frames, int H, int W,
+                                   int window_len, int model_order, const float* ref_phase,
+                                   float* out_phase, unsigned long long* d_counters,
+                                   void* stream);
+
+/* Static, never-NULL description of a status code. */
+const char* bos_strerror(int code);
+
+/* ABI version: (major << 16) | minor. */
+int bos_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BOS_ROOTMUSIC_H */

@@ -263,7 +263,7 @@ def _estimate_pixels(frame, py, px, M):
 
 
 def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_phase=None,
-                pixels=None, threads: int | None = None, chunk: int = 2048):
+                pixels=None, threads: int | None = None, chunk: int | None = None):
     """Phase map of one frame: Algorithm 1 at every pixel (or at ``pixels=(py, px)``).
 
     ref_phase: None → raw α (wrapped); else out = wrap(α - ref_phase) [R7], where
@@ -285,6 +285,9 @@ def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_ph
     else:
         py, px = (np.asarray(p, dtype=np.int64).ravel() for p in pixels)
     n = py.size
+    nthreads = threads or default_threads()
+    if chunk is None:   # static partition depending on n only (not on the thread count)
+        chunk = int(min(2048, max(128, -(-n // 32))))
     alpha = np.empty(n, dtype=np.float64)
     flags = np.empty(n, dtype=np.uint8)
     bounds = list(range(0, n, chunk)) + [n]
@@ -293,7 +296,6 @@ def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_ph
         s, e = bounds[j], bounds[j + 1]
         alpha[s:e], flags[s:e] = _estimate_pixels(frame, py[s:e], px[s:e], M)
 
-    nthreads = threads or default_threads()
     if nthreads == 1 or len(bounds) <= 2:
         for j in range(len(bounds) - 1):
             work(j)

@@ -1,0 +1,209 @@
+"""Thin ctypes binding of libbosrm.so (C ABI: include/bos_rootmusic.h).
+
+Argument marshalling only: every step of the demodulation runs in the library's sm_100a
+kernels.  Functions carry the C names.  There is no fallback: if the library is missing,
+or a tensor is not where the ABI says it must be, the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libbosrm.so")
+
+BOS_OK = 0
+BOS_ERR_INVALID_ARG = -1
+BOS_ERR_UNSUPPORTED = -2
+BOS_ERR_CUDA = -3
+
+FLAG_NONCONVERGED = 1 << 0
+FLAG_AMBIGUOUS = 1 << 1
+FLAG_SMALL_GAP = 1 << 2
+FLAG_LOW_AMPLITUDE = 1 << 3
+FLAG_NONFINITE = 1 << 4
+FLAG_BORDER = 1 << 5
+
+WINDOW_LEN_MIN = 3
+WINDOW_LEN_MAX = 16
+MODEL_ORDER = 3
+
+# name -> (restype, argtypes); must match include/bos_rootmusic.h
+_VP, _I, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+SIGNATURES = {
+    "bos_rootmusic_demod": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
+    "bos_rootmusic_demod_stack": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
+    "bos_rootmusic_host_workspace_bytes": (_SZ, [_I, _I, _I, _I]),
+    "bos_rootmusic_demod_stack_host": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _SZ, _I, _VP]),
+    "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
+    "bos_strerror": (ctypes.c_char_p, [_I]),
+    "bos_abi_version": (_I, []),
+}
+
+_lib = None
+
+
+class BosError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {bos_strerror(code)} (code {code})")
+        self.code = code
+
+
+def lib() -> ctypes.CDLL:
+    """Load libbosrm.so (built in-tree by paper_1910_11872_b200.build); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with "
+                               "`python -m paper_1910_11872_b200.build` (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def bos_strerror(code: int) -> str:
+    return lib().bos_strerror(int(code)).decode()
+
+
+def bos_abi_version() -> int:
+    return lib().bos_abi_version()
+
+
+def _check(rc: int, where: str):
+    if rc != BOS_OK:
+        raise BosError(rc, where)
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _dev_tensor(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _frames3(frames: torch.Tensor) -> torch.Tensor:
+    if frames.dim() == 2:
+        frames = frames.unsqueeze(0)
+    if frames.dim() != 3:
+        raise ValueError("frames must be [H,W] or [T,H,W]")
+    return frames
+
+
+def bos_rootmusic_demod(frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
+                        ref_phase: torch.Tensor | None = None, out_phase: torch.Tensor | None = None,
+                        flags: torch.Tensor | bool | None = None, stream=None):
+    """Demodulate complex64 CUDA frames [T,H,W] (or [H,W]) → (phase float32, flags uint8|None).
+
+    ``flags=True`` allocates the flag plane; a tensor is written in place; None skips it."""
+    frames = _dev_tensor(_frames3(frames), torch.complex64, "frames")
+    T, H, W = frames.shape
+    if out_phase is None:
+        out_phase = torch.empty(T, H, W, dtype=torch.float32, device=frames.device)
+    _dev_tensor(out_phase, torch.float32, "out_phase")
+    if flags is True:
+        flags = torch.empty(T, H, W, dtype=torch.uint8, device=frames.device)
+    elif flags is False:
+        flags = None
+    if flags is not None:
+        _dev_tensor(flags, torch.uint8, "flags")
+    if ref_phase is not None:
+        _dev_tensor(ref_phase, torch.float32, "ref_phase")
+    rc = lib().bos_rootmusic_demod(
+        frames.data_ptr(), T, H, W, int(window_len), int(model_order),
+        ref_phase.data_ptr() if ref_phase is not None else None, out_phase.data_ptr(),
+        flags.data_ptr() if flags is not None else None, _stream_ptr(stream))
+    _check(rc, "bos_rootmusic_demod")
+    return out_phase, flags
+
+
+def bos_rootmusic_demod_stack(frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
+                              ref_index: int = 0, ref_phase_out: torch.Tensor | None = None,
+                              out_phase: torch.Tensor | None = None, flags=None, stream=None):
+    """Time-lapse stack against frames[ref_index] → (phase, flags|None, ref_phase)."""
+    frames = _dev_tensor(_frames3(frames), torch.complex64, "frames")
+    T, H, W = frames.shape
+    dev = frames.device
+    if ref_phase_out is None:
+        ref_phase_out = torch.empty(H, W, dtype=torch.float32, device=dev)
+    if out_phase is None:
+        out_phase = torch.empty(T, H, W, dtype=torch.float32, device=dev)
+    if flags is True:
+        flags = torch.empty(T, H, W, dtype=torch.uint8, device=dev)
+    elif flags is False:
+        flags = None
+    _dev_tensor(ref_phase_out, torch.float32, "ref_phase_out")
+    _dev_tensor(out_phase, torch.float32, "out_phase")
+    if flags is not None:
+        _dev_tensor(flags, torch.uint8, "flags")
+    rc = lib().bos_rootmusic_demod_stack(
+        frames.data_ptr(), T, H, W, int(window_len), int(model_order), int(ref_index),
+        ref_phase_out.data_ptr(), out_phase.data_ptr(), flags.data_ptr() if flags is not None else None,
+        _stream_ptr(stream))
+    _check(rc, "bos_rootmusic_demod_stack")
+    return out_phase, flags, ref_phase_out
+
+
+def bos_rootmusic_host_workspace_bytes(H: int, W: int, chunk_frames: int, with_flags: bool) -> int:
+    return int(lib().bos_rootmusic_host_workspace_bytes(int(H), int(W), int(chunk_frames), int(bool(with_flags))))
+
+
+def bos_rootmusic_demod_stack_host(h_frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
+                                   ref_index: int = 0, h_out_phase: torch.Tensor | None = None,
+                                   h_flags=None, workspace: torch.Tensor | None = None, chunk_frames: int = 8,
+                                   stream=None, device=None):
+    """Host-buffer stack demod: CPU complex64 [T,H,W] (pinned for overlap) → CPU phase/flags.
+    The device workspace is a caller-owned CUDA uint8 tensor (allocated here if None).
+    Results are valid after ``stream`` (default: current stream) synchronises."""
+    if h_frames.device.type != "cpu" or h_frames.dtype != torch.complex64 or not h_frames.is_contiguous():
+        raise ValueError("h_frames must be a contiguous CPU complex64 tensor")
+    h_frames = _frames3(h_frames)
+    T, H, W = h_frames.shape
+    pin = h_frames.is_pinned()
+    if h_out_phase is None:
+        h_out_phase = torch.empty(T, H, W, dtype=torch.float32, pin_memory=pin)
+    if h_flags is True:
+        h_flags = torch.empty(T, H, W, dtype=torch.uint8, pin_memory=pin)
+    elif h_flags is False:
+        h_flags = None
+    need = bos_rootmusic_host_workspace_bytes(H, W, min(chunk_frames, T), h_flags is not None)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=device or "cuda")
+    _dev_tensor(workspace, torch.uint8, "workspace")
+    rc = lib().bos_rootmusic_demod_stack_host(
+        h_frames.data_ptr(), T, H, W, int(window_len), int(model_order), int(ref_index),
+        h_out_phase.data_ptr(), h_flags.data_ptr() if h_flags is not None else None,
+        workspace.data_ptr(), workspace.numel(), int(chunk_frames), _stream_ptr(stream))
+    _check(rc, "bos_rootmusic_demod_stack_host")
+    return h_out_phase, h_flags
+
+
+def bos_rootmusic_iteration_counts(frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
+                                   ref_phase: torch.Tensor | None = None, stream=None):
+    """Run the counting variant; returns dict(pixels, power_its, aberth_y, aberth_x) (host ints)."""
+    frames = _dev_tensor(_frames3(frames), torch.complex64, "frames")
+    T, H, W = frames.shape
+    out = torch.empty(T, H, W, dtype=torch.float32, device=frames.device)
+    cnt = torch.zeros(4, dtype=torch.int64, device=frames.device)
+    rc = lib().bos_rootmusic_iteration_counts(
+        frames.data_ptr(), T, H, W, int(window_len), int(model_order),
+        ref_phase.data_ptr() if ref_phase is not None else None, out.data_ptr(), cnt.data_ptr(),
+        _stream_ptr(stream))
+    _check(rc, "bos_rootmusic_iteration_counts")
+    c = cnt.cpu().tolist()
+    return dict(pixels=c[0], power_its=c[1], aberth_y=c[2], aberth_x=c[3], out=out)

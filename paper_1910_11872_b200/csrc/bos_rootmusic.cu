@@ -1,0 +1,241 @@
+// bos_rootmusic.cu — host side of libbosrm.so: argument validation, M-specialised kernel
+// dispatch, the time-lapse stack driver and the pipelined host-buffer driver.
+// The C ABI is declared (and documented) in include/bos_rootmusic.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "bos_rootmusic.h"
+#include "launch.h"
+#include "template_roots.h"
+
+namespace {
+
+using LaunchFn = cudaError_t (*)(const float2*, int, int, int, const float*, float*, uint8_t*,
+                                 unsigned long long*, cudaStream_t);
+
+template <bool COUNT>
+LaunchFn pick(int M) {
+    switch (M) {
+        case 3: return bos::launch_demod<3, COUNT>;
+        case 4: return bos::launch_demod<4, COUNT>;
+        case 5: return bos::launch_demod<5, COUNT>;
+        case 6: return bos::launch_demod<6, COUNT>;
+        case 7: return bos::launch_demod<7, COUNT>;
+        case 8: return bos::launch_demod<8, COUNT>;
+        case 9: return bos::launch_demod<9, COUNT>;
+        case 10: return bos::launch_demod<10, COUNT>;
+        case 11: return bos::launch_demod<11, COUNT>;
+        case 12: return bos::launch_demod<12, COUNT>;
+        case 13: return bos::launch_demod<13, COUNT>;
+        case 14: return bos::launch_demod<14, COUNT>;
+        case 15: return bos::launch_demod<15, COUNT>;
+        case 16: return bos::launch_demod<16, COUNT>;
+        default: return nullptr;
+    }
+}
+static_assert(BOS_WINDOW_LEN_MAX <= BOS_TEMPLATE_M_MAX, "template table too small");
+
+// 1 if p is a device (or managed) pointer, 0 otherwise.
+int is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+int check_common(int n_frames, int H, int W, int window_len, int model_order) {
+    if (model_order != BOS_MODEL_ORDER) return BOS_ERR_UNSUPPORTED;
+    if (window_len < BOS_WINDOW_LEN_MIN) return BOS_ERR_INVALID_ARG;
+    if (window_len > BOS_WINDOW_LEN_MAX) return BOS_ERR_UNSUPPORTED;
+    if (n_frames < 1 || H < window_len || W < window_len) return BOS_ERR_INVALID_ARG;
+    return BOS_OK;
+}
+
+int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_len, int model_order,
+               const float* ref_phase, float* out_phase, uint8_t* flags, unsigned long long* counters,
+               void* stream, bool check_ptrs) {
+    int rc = check_common(n_frames, H, W, window_len, model_order);
+    if (rc != BOS_OK) return rc;
+    if (frames == nullptr || out_phase == nullptr) return BOS_ERR_INVALID_ARG;
+    const size_t plane = (size_t)H * (size_t)W;
+    const size_t n = plane * (size_t)n_frames;
+    if (overlaps(frames, n * sizeof(bos_cf32), out_phase, n * sizeof(float))) return BOS_ERR_INVALID_ARG;
+    if (ref_phase != nullptr && overlaps(ref_phase, plane * sizeof(float), out_phase, n * sizeof(float)))
+        return BOS_ERR_INVALID_ARG;
+    if (flags != nullptr && (overlaps(flags, n, out_phase, n * sizeof(float)) ||
+                             overlaps(flags, n, frames, n * sizeof(bos_cf32))))
+        return BOS_ERR_INVALID_ARG;
+    if (check_ptrs) {
+        if (!is_device_ptr(frames) || !is_device_ptr(out_phase)) return BOS_ERR_INVALID_ARG;
+        if (ref_phase != nullptr && !is_device_ptr(ref_phase)) return BOS_ERR_INVALID_ARG;
+        if (flags != nullptr && !is_device_ptr(flags)) return BOS_ERR_INVALID_ARG;
+    }
+    LaunchFn fn = counters ? pick<true>(window_len) : pick<false>(window_len);
+    if (fn == nullptr) return BOS_ERR_UNSUPPORTED;
+    const cudaError_t e = fn(reinterpret_cast<const float2*>(frames), n_frames, H, W, ref_phase, out_phase,
+                             flags, counters, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+}  // namespace
+
+extern "C" {
+
+int bos_abi_version(void) { return (1 << 16) | 0; }
+
+const char* bos_strerror(int code) {
+    switch (code) {
+        case BOS_OK: return "ok";
+        case BOS_ERR_INVALID_ARG: return "invalid argument (NULL pointer, size, aliasing or host/device pointer)";
+        case BOS_ERR_UNSUPPORTED: return "unsupported (model_order must be 3; window_len outside the instantiated range)";
+        case BOS_ERR_CUDA: return "CUDA runtime error or kernel launch failure";
+        default: return "unknown bos_rootmusic status code";
+    }
+}
+
+int bos_rootmusic_demod(const bos_cf32* frames, int n_frames, int H, int W, int window_len, int model_order,
+                        const float* ref_phase, float* out_phase, uint8_t* flags, void* stream) {
+    return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, flags, nullptr,
+                      stream, true);
+}
+
+int bos_rootmusic_iteration_counts(const bos_cf32* frames, int n_frames, int H, int W, int window_len,
+                                   int model_order, const float* ref_phase, float* out_phase,
+                                   unsigned long long* d_counters, void* stream) {
+    if (d_counters == nullptr || !is_device_ptr(d_counters)) return BOS_ERR_INVALID_ARG;
+    return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, nullptr,
+                      d_counters, stream, true);
+}
+
+int bos_rootmusic_demod_stack(const bos_cf32* frames, int n_frames, int H, int W, int window_len,
+                              int model_order, int ref_index, float* ref_phase_out, float* out_phase,
+                              uint8_t* flags, void* stream) {
+    int rc = check_common(n_frames, H, W, window_len, model_order);
+    if (rc != BOS_OK) return rc;
+    if (ref_index < 0 || ref_index >= n_frames || ref_phase_out == nullptr || frames == nullptr)
+        return BOS_ERR_INVALID_ARG;
+    const size_t plane = (size_t)H * (size_t)W;
+    if (overlaps(ref_phase_out, plane * sizeof(float), frames, plane * (size_t)n_frames * sizeof(bos_cf32)))
+        return BOS_ERR_INVALID_ARG;
+    if (!is_device_ptr(ref_phase_out)) return BOS_ERR_INVALID_ARG;
+    rc = demod_impl(frames + (size_t)ref_index * plane, 1, H, W, window_len, model_order, nullptr, ref_phase_out,
+                    nullptr, nullptr, stream, true);
+    if (rc != BOS_OK) return rc;
+    return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase_out, out_phase, flags, nullptr,
+                      stream, true);
+}
+
+size_t bos_rootmusic_host_workspace_bytes(int H, int W, int chunk_frames, int with_flags) {
+    if (H < 1 || W < 1 || chunk_frames < 1) return 0;
+    const size_t plane = (size_t)H * (size_t)W;
+    const size_t c = (size_t)chunk_frames * plane;
+    size_t slot = align_up(c * sizeof(bos_cf32)) + align_up(c * sizeof(float)) + (with_flags ? align_up(c) : 0);
+    return align_up(plane * sizeof(float)) + 2 * slot;
+}
+
+int bos_rootmusic_demod_stack_host(const bos_cf32* h_frames, int n_frames, int H, int W, int window_len,
+                                   int model_order, int ref_index, float* h_out_phase, uint8_t* h_flags,
+                                   void* d_workspace, size_t workspace_bytes, int chunk_frames, void* stream) {
+    int rc = check_common(n_frames, H, W, window_len, model_order);
+    if (rc != BOS_OK) return rc;
+    if (h_frames == nullptr || h_out_phase == nullptr || d_workspace == nullptr || chunk_frames < 1 ||
+        ref_index < 0 || ref_index >= n_frames)
+        return BOS_ERR_INVALID_ARG;
+    if (is_device_ptr(h_frames) || is_device_ptr(h_out_phase) || (h_flags && is_device_ptr(h_flags)) ||
+        !is_device_ptr(d_workspace))
+        return BOS_ERR_INVALID_ARG;
+    chunk_frames = std::min(chunk_frames, n_frames);
+    const bool wf = h_flags != nullptr;
+    if (workspace_bytes < bos_rootmusic_host_workspace_bytes(H, W, chunk_frames, wf)) return BOS_ERR_INVALID_ARG;
+
+    const size_t plane = (size_t)H * (size_t)W;
+    const size_t c = (size_t)chunk_frames * plane;
+    char* base = static_cast<char*>(d_workspace);
+    float* d_ref = reinterpret_cast<float*>(base);
+    base += align_up(plane * sizeof(float));
+    bos_cf32* d_frames[2];
+    float* d_out[2];
+    uint8_t* d_flags[2] = {nullptr, nullptr};
+    for (int s = 0; s < 2; ++s) {
+        d_frames[s] = reinterpret_cast<bos_cf32*>(base);
+        base += align_up(c * sizeof(bos_cf32));
+        d_out[s] = reinterpret_cast<float*>(base);
+        base += align_up(c * sizeof(float));
+        if (wf) {
+            d_flags[s] = reinterpret_cast<uint8_t*>(base);
+            base += align_up(c);
+        }
+    }
+
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_ref = nullptr, ev_end[2] = {nullptr, nullptr};
+    cudaError_t e = cudaSuccess;
+    auto ok = [&](cudaError_t x) {
+        if (e == cudaSuccess && x != cudaSuccess) e = x;
+        return e == cudaSuccess;
+    };
+    ok(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
+    ok(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+    ok(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    ok(cudaEventCreateWithFlags(&ev_ref, cudaEventDisableTiming));
+    ok(cudaEventCreateWithFlags(&ev_end[0], cudaEventDisableTiming));
+    ok(cudaEventCreateWithFlags(&ev_end[1], cudaEventDisableTiming));
+    if (e == cudaSuccess) {
+        ok(cudaEventRecord(ev_start, user));
+        ok(cudaStreamWaitEvent(st[0], ev_start, 0));
+        ok(cudaStreamWaitEvent(st[1], ev_start, 0));
+        // reference frame → d_ref (raw α), on stream 0
+        ok(cudaMemcpyAsync(d_frames[0], h_frames + (size_t)ref_index * plane, plane * sizeof(bos_cf32),
+                           cudaMemcpyHostToDevice, st[0]));
+        if (e == cudaSuccess) {
+            rc = demod_impl(d_frames[0], 1, H, W, window_len, model_order, nullptr, d_ref, nullptr, nullptr, st[0],
+                            false);
+            if (rc != BOS_OK && e == cudaSuccess) e = cudaErrorLaunchFailure;
+        }
+        ok(cudaEventRecord(ev_ref, st[0]));
+        ok(cudaStreamWaitEvent(st[1], ev_ref, 0));
+        // ping-pong chunks: H2D(k) ‖ kernel(k−1) ‖ D2H(k−2) across the two streams
+        for (int f0 = 0, k = 0; f0 < n_frames && e == cudaSuccess; f0 += chunk_frames, ++k) {
+            const int s = k & 1;
+            const int nk = std::min(chunk_frames, n_frames - f0);
+            const size_t cnt = (size_t)nk * plane;
+            ok(cudaMemcpyAsync(d_frames[s], h_frames + (size_t)f0 * plane, cnt * sizeof(bos_cf32),
+                               cudaMemcpyHostToDevice, st[s]));
+            if (e != cudaSuccess) break;
+            rc = demod_impl(d_frames[s], nk, H, W, window_len, model_order, d_ref, d_out[s], d_flags[s], nullptr,
+                            st[s], false);
+            if (rc != BOS_OK) {
+                e = cudaErrorLaunchFailure;
+                break;
+            }
+            ok(cudaMemcpyAsync(h_out_phase + (size_t)f0 * plane, d_out[s], cnt * sizeof(float),
+                               cudaMemcpyDeviceToHost, st[s]));
+            if (wf) ok(cudaMemcpyAsync(h_flags + (size_t)f0 * plane, d_flags[s], cnt, cudaMemcpyDeviceToHost, st[s]));
+        }
+        cudaEventRecord(ev_end[0], st[0]);
+        cudaEventRecord(ev_end[1], st[1]);
+        cudaStreamWaitEvent(user, ev_end[0], 0);
+        cudaStreamWaitEvent(user, ev_end[1], 0);
+    }
+    for (int s = 0; s < 2; ++s) {
+        if (st[s]) cudaStreamDestroy(st[s]);   // deferred until queued work completes
+        if (ev_end[s]) cudaEventDestroy(ev_end[s]);
+    }
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_ref) cudaEventDestroy(ev_ref);
+    return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
+}
+
+}  // extern "C"

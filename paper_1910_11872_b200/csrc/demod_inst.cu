@@ -1,0 +1,28 @@
+// demod_inst.cu — explicit instantiation of the demod kernel launcher for one window size
+// M = BOS_INST_M (the build compiles this file once per M, in parallel).
+#include <algorithm>
+
+#include "demod_kernel.cuh"
+#include "launch.h"
+
+#ifndef BOS_INST_M
+#error "compile with -DBOS_INST_M=<window_len>"
+#endif
+
+namespace bos {
+
+template <int M, bool COUNT>
+cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+                         uint8_t* flags, unsigned long long* counters, cudaStream_t s) {
+    const dim3 block(kBX, kBY, 1);
+    const dim3 grid((unsigned)((W + kBX - 1) / kBX), (unsigned)((H + kBY - 1) / kBY),
+                    (unsigned)std::min(n_frames, 65535));
+    demod_kernel<M, COUNT><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, counters);
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_demod<BOS_INST_M, false>(const float2*, int, int, int, const float*, float*, uint8_t*,
+                                                     unsigned long long*, cudaStream_t);
+template cudaError_t launch_demod<BOS_INST_M, true>(const float2*, int, int, int, const float*, float*, uint8_t*,
+                                                    unsigned long long*, cudaStream_t);
+}  // namespace bos

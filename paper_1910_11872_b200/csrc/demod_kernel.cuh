@@ -1,0 +1,365 @@
+// demod_kernel.cuh — sm_100a windowed root-MUSIC demodulation kernel (thread per pixel).
+//
+// One CTA = a 32×4 pixel tile of one frame.  The CTA stages the (4+M−1)×(32+M−1) complex
+// window halo of its tile in shared memory once (every HBM byte of the frame is read once
+// per frame, the overlap between the M² windows of neighbouring pixels is served from
+// SMEM), then each thread runs the whole per-pixel chain of Algorithm 1 in
+// registers, fused with the reference-phase difference and the flag store:
+//
+//   a2  R_y = Γ_w Γ_w^H (lower triangle, FP32)                            Eq.(4)
+//   a3  u_1: power iteration on R_y from the lag-1 tone estimate; v_1 ∝ Γ_w^H u_1
+//       (SVD identity), so U_nU_n^H = I − u_1u_1^H, V_nV_n^H = I − v_1v_1^H  Eqs.(7)-(11),(14)
+//   a4  P(z) coefficients = diagonal sums of I − qq^H (autocorrelation of q)  Eqs.(12),(13)
+//   a5  all 2M−2 roots by Aberth–Ehrlich from rotated noise-free templates; root
+//       minimising |ln|z|| (≡ "closest to the unit circle, inside", P:L208 [R6])
+//   a6  α = ∠ Σ_i conj(ẑ_y)^{o_i} Σ_k Γ_w(i,k) ẑ_x^{o_k}   (ẑ = z/|z| = e^{jω_y}, e^{-jω_x})
+//   a7  out = wrap(α − φ_ref) ∈ (−π, π]; flags
+//
+// No tensor cores: these are tiny per-pixel systems (BASELINE north_star).  The path is
+// FP32-FMA / MUFU bound.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "template_roots.h"
+
+namespace bos {
+
+constexpr int kBX = 32;               // pixels per CTA along x (one warp per row)
+constexpr int kBY = 4;                // rows per CTA
+constexpr int kThreads = kBX * kBY;
+
+constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyond)
+constexpr float kPowerTol = 4e-13f;   // ‖u_{k+1} − u_k‖² stop
+constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
+constexpr float kAberthTol2 = 1e-12f; // max_i |Δz_i|² stop
+constexpr float kCosTauOmega = 0.99995000042f;  // cos(1e-2): "distinct frequency" test
+constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
+constexpr float kLowAmp = 1e-4f;      // LOW_AMPLITUDE threshold
+
+enum : uint8_t {
+    kFlagNonconverged = 1u << 0,
+    kFlagAmbiguous = 1u << 1,
+    kFlagLowAmplitude = 1u << 3,
+    kFlagNonfinite = 1u << 4,
+    kFlagBorder = 1u << 5,
+};
+
+// ---------------------------------------------------------------- complex helpers (FP32)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// a*b + c
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 c) {
+    return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, c.y)));
+}
+// a*conj(b) + c
+__device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 c) {
+    return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, c.x)), fmaf(a.y, b.x, fmaf(-a.x, b.y, c.y)));
+}
+__device__ __forceinline__ float cabs2(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// 1/a with one MUFU.RCP (approximate reciprocal of |a|²)
+__device__ __forceinline__ float2 crcp(float2 a) {
+    const float r = __fdividef(1.0f, cabs2(a));
+    return make_float2(a.x * r, -a.y * r);
+}
+// a/b
+__device__ __forceinline__ float2 cdiv(float2 a, float2 b) {
+    const float r = __fdividef(1.0f, cabs2(b));
+    return make_float2(fmaf(a.x, b.x, a.y * b.y) * r, fmaf(a.y, b.x, -a.x * b.y) * r);
+}
+
+template <int M>
+__device__ __forceinline__ constexpr int tri_off(int i, int j) {  // strict lower triangle, j < i
+    return i * (i - 1) / 2 + j;
+}
+
+// Roots of P(z) = Σ_{n=0}^{N} c_n z^n (N = 2M−2) by Gauss–Seidel Aberth–Ehrlich iteration.
+// Returns the number of sweeps; `ok` = converged (tolerance) or stagnated at FP32 noise.
+template <int N>
+__device__ __forceinline__ int aberth(const float2 (&c)[N + 1], float2 (&z)[N], bool& ok) {
+    float prev = CUDART_INF_F;
+    int it = 0;
+    ok = false;
+    for (; it < kAberthMaxIt; ++it) {
+        float maxw = 0.0f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const float2 zi = z[i];
+            float2 p = c[N];
+            float2 dp = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = N - 1; k >= 0; --k) {
+                dp = cfma(dp, zi, p);
+                p = cfma(p, zi, c[k]);
+            }
+            const float2 ratio = cdiv(p, dp);          // Newton step P/P'
+            float2 s = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                if (j != i) s = cadd(s, crcp(csub(zi, z[j])));
+            }
+            // w = ratio / (1 − ratio·s)
+            const float2 den = make_float2(1.0f - (ratio.x * s.x - ratio.y * s.y),
+                                           -(ratio.x * s.y + ratio.y * s.x));
+            const float2 w = cdiv(ratio, den);
+            z[i] = csub(zi, w);
+            maxw = fmaxf(maxw, cabs2(w));
+        }
+        if (maxw < kAberthTol2) { ok = true; ++it; break; }
+        // Multiple (noise-free, double) roots converge linearly down to the FP32 noise
+        // floor (≈√ε); stop once a sweep no longer makes progress there.
+        if (it >= 4 && maxw < 1e-6f && maxw > 0.9f * prev) { ok = true; ++it; break; }
+        prev = maxw;
+    }
+    return it;
+}
+
+// Root closest to the unit circle (min |ln|z||, via the monotone tanh(|ln r|) =
+// |r²−1|/(r²+1)) and the margin to the best root of a different frequency.
+template <int N>
+__device__ __forceinline__ float2 select_root(const float2 (&z)[N], float& margin) {
+    float best = CUDART_INF_F;
+    float2 zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const float r2 = cabs2(z[i]);
+        const float d = fabsf(r2 - 1.0f) / (r2 + 1.0f);
+        if (d < best) { best = d; zb = z[i]; }
+    }
+    const float rb = sqrtf(cabs2(zb));
+    float second = CUDART_INF_F;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const float r2 = cabs2(z[i]);
+        const float d = fabsf(r2 - 1.0f) / (r2 + 1.0f);
+        const float dot = fmaf(z[i].x, zb.x, z[i].y * zb.y);        // Re(z_i conj(z_b))
+        if (dot < kCosTauOmega * sqrtf(r2) * rb) second = fminf(second, d);
+    }
+    // |ln r| = atanh(d)
+    const float a1 = 0.5f * __logf((1.0f + best) / (1.0f - best));
+    const float a2 = second < 1.0f ? 0.5f * __logf((1.0f + second) / (1.0f - second)) : CUDART_INF_F;
+    margin = a2 - a1;
+    return zb;
+}
+
+// Coefficients of P(z) = z^{M−1} q^H(z)(I − qq^H)q(z) for a unit vector q:
+// c_{M−1} = M − ‖q‖², c_{M−1+d} = −r_d, c_{M−1−d} = −conj(r_d), r_d = Σ_i q_i conj(q_{i+d}).
+// Also returns the rotation e^{jω̂} = conj(r_1)/|r_1| (tone estimate for the template).
+template <int M>
+__device__ __forceinline__ float2 music_coeffs(const float2 (&q)[M], float2 (&c)[2 * M - 1]) {
+    float n2 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < M; ++i) n2 += cabs2(q[i]);
+    c[M - 1] = make_float2(float(M) - n2, 0.0f);
+    float2 r1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int d = 1; d < M; ++d) {
+        float2 r = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i + d < M; ++i) r = cfmac(q[i], q[i + d], r);
+        c[M - 1 + d] = make_float2(-r.x, -r.y);
+        c[M - 1 - d] = make_float2(-r.x, r.y);
+        if (d == 1) r1 = r;
+    }
+    const float n = cabs2(r1);
+    if (!(n > 0.0f)) return make_float2(1.0f, 0.0f);
+    const float inv = rsqrtf(n);
+    return make_float2(r1.x * inv, -r1.y * inv);
+}
+
+template <int M, bool COUNT>
+__global__ void __launch_bounds__(kThreads)
+demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
+             const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
+             unsigned long long* __restrict__ counters) {
+    constexpr int N = 2 * M - 2;                 // polynomial degree
+    constexpr int O0 = (M - 1) / 2;              // o_i = i − O0  [R2]
+    constexpr int TW = kBX + M - 1;
+    constexpr int TH = kBY + M - 1;
+    constexpr int NOFF = M * (M - 1) / 2;
+    __shared__ float2 tile[TH * TW];
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+    const int px = x0 + tx, py = y0 + ty;
+    const size_t plane = (size_t)H * (size_t)W;
+
+    for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
+        const float2* __restrict__ frame = frames + (size_t)f * plane;
+        // ---- a1: stage the clamped halo tile (Eq.(2) window support, [R1] clamp) ----
+        for (int idx = ty * kBX + tx; idx < TH * TW; idx += kThreads) {
+            const int r = idx / TW, cc = idx - r * TW;
+            const int gy = min(max(y0 - O0 + r, 0), H - 1);
+            const int gx = min(max(x0 - O0 + cc, 0), W - 1);
+            tile[idx] = __ldg(frame + (size_t)gy * W + gx);
+        }
+        __syncthreads();
+
+        if (px < W && py < H) {
+            const float2* win = tile + ty * TW + tx;   // Γ_w(i,k) = win[i*TW + k]
+            uint8_t fl = 0;
+            if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
+                fl |= kFlagBorder;
+
+            // ---- a2: R_y = Γ_w Γ_w^H, diagonal (real) + strict lower triangle ----
+            float Rd[M];
+            float2 Ro[NOFF > 0 ? NOFF : 1];
+#pragma unroll
+            for (int i = 0; i < M; ++i) Rd[i] = 0.0f;
+#pragma unroll
+            for (int t = 0; t < NOFF; ++t) Ro[t] = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+                float2 col[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) col[i] = win[i * TW + k];
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    Rd[i] = fmaf(col[i].x, col[i].x, fmaf(col[i].y, col[i].y, Rd[i]));
+#pragma unroll
+                    for (int j = 0; j < i; ++j) Ro[tri_off<M>(i, j)] = cfmac(col[i], col[j], Ro[tri_off<M>(i, j)]);
+                }
+            }
+            float trace = 0.0f;
+#pragma unroll
+            for (int i = 0; i < M; ++i) trace += Rd[i];
+
+            float result;
+            int n_pow = 0, n_aby = 0, n_abx = 0;
+            if (!isfinite(trace)) {
+                fl |= kFlagNonfinite;
+                result = CUDART_NAN_F;
+            } else {
+                // ---- a3: dominant eigenvector of R_y by power iteration ----
+                // start: u_i = e^{jω̂ i}/√M with e^{jω̂} ∝ Σ_i R[i+1][i] (lag-1 correlation)
+                float2 r1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, Ro[tri_off<M>(i + 1, i)]);
+                float2 e = make_float2(1.0f, 0.0f);
+                if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+                float2 u[M];
+                u[0] = make_float2(rsqrtf(float(M)), 0.0f);
+#pragma unroll
+                for (int i = 1; i < M; ++i) u[i] = cmul(u[i - 1], e);
+                bool pow_ok = false;
+                for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                    float2 y[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        float2 acc = make_float2(Rd[i] * u[i].x, Rd[i] * u[i].y);
+#pragma unroll
+                        for (int j = 0; j < i; ++j) acc = cfma(Ro[tri_off<M>(i, j)], u[j], acc);
+#pragma unroll
+                        for (int j = i + 1; j < M; ++j) acc = cfmac(u[j], Ro[tri_off<M>(j, i)], acc);
+                        y[i] = acc;
+                    }
+                    float nrm2 = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) nrm2 += cabs2(y[i]);
+                    const float inv = rsqrtf(nrm2);
+                    float diff = 0.0f;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        const float2 yn = cscale(y[i], inv);
+                        diff += cabs2(csub(yn, u[i]));
+                        u[i] = yn;
+                    }
+                    ++n_pow;
+                    if (diff < kPowerTol) { pow_ok = true; break; }
+                }
+                // v_1 ∝ Γ_w^H u_1
+                float2 v[M];
+                float vn = 0.0f;
+#pragma unroll
+                for (int k = 0; k < M; ++k) {
+                    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int i = 0; i < M; ++i) acc = cfmac(u[i], win[i * TW + k], acc);  // u_i conj(Γ)
+                    v[k] = acc;
+                    vn += cabs2(acc);
+                }
+                const float vinv = rsqrtf(vn);
+#pragma unroll
+                for (int k = 0; k < M; ++k) v[k] = cscale(v[k], vinv);
+
+                // ---- a4 + a5, y axis then x axis ----
+                float2 zy, zx;
+                float my, mx;
+                bool aby_ok, abx_ok;
+                {
+                    float2 c[N + 1];
+                    const float2 rot = music_coeffs<M>(u, c);
+                    float2 z[N];
+#pragma unroll
+                    for (int j = 0; j < N; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
+                    n_aby = aberth<N>(c, z, aby_ok);
+                    zy = select_root<N>(z, my);
+                }
+                {
+                    float2 c[N + 1];
+                    const float2 rot = music_coeffs<M>(v, c);
+                    float2 z[N];
+#pragma unroll
+                    for (int j = 0; j < N; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
+                    n_abx = aberth<N>(c, z, abx_ok);
+                    zx = select_root<N>(z, mx);
+                }
+                if (!pow_ok || !aby_ok || !abx_ok || !isfinite(zy.x + zy.y + zx.x + zx.y))
+                    fl |= kFlagNonconverged;
+                if (fminf(my, mx) < kTauSel) fl |= kFlagAmbiguous;
+
+                // ---- a6: Eq.(15) least-squares phase at the target pixel ----
+                // ẑ_x = e^{-jω_x}, ẑ_y = e^{jω_y}; basis e^{-j(ω_x o_k + ω_y o_i)} = ẑ_x^{o_k} conj(ẑ_y)^{o_i}
+                const float2 hx = cscale(zx, rsqrtf(cabs2(zx)));
+                const float2 hy = cscale(zy, rsqrtf(cabs2(zy)));
+                float2 tw[M];
+                {
+                    float2 p = make_float2(1.0f, 0.0f);
+#pragma unroll
+                    for (int k = 0; k < O0; ++k) p = cmul(p, cconj(hx));
+                    tw[0] = p;
+#pragma unroll
+                    for (int k = 1; k < M; ++k) tw[k] = cmul(tw[k - 1], hx);
+                }
+                float2 q = make_float2(1.0f, 0.0f);
+#pragma unroll
+                for (int i = 0; i < O0; ++i) q = cmul(q, hy);
+                float2 csum = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    float2 row = make_float2(0.0f, 0.0f);
+#pragma unroll
+                    for (int k = 0; k < M; ++k) row = cfma(win[i * TW + k], tw[k], row);
+                    csum = cfma(row, q, csum);
+                    q = cmul(q, cconj(hy));
+                }
+                if (!(cabs2(csum) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
+                float a = atan2f(csum.y, csum.x);
+                // ---- a7: reference difference, wrap into (−π, π] ----
+                if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
+                if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
+                if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
+                result = a;
+            }
+            const size_t o = (size_t)f * plane + (size_t)py * W + px;
+            out[o] = result;
+            if (flags != nullptr) flags[o] = fl;
+            if (COUNT) {
+                atomicAdd(counters + 0, 1ull);
+                atomicAdd(counters + 1, (unsigned long long)n_pow);
+                atomicAdd(counters + 2, (unsigned long long)n_aby);
+                atomicAdd(counters + 3, (unsigned long long)n_abx);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace bos

@@ -1,0 +1,11 @@
+// launch.h — declarations of the per-M kernel launchers (one object file per window size,
+// compiled in parallel from demod_inst.cu with -DBOS_INST_M=<M>).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bos {
+template <int M, bool COUNT>
+cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+                         uint8_t* flags, unsigned long long* counters, cudaStream_t s);
+}  // namespace bos

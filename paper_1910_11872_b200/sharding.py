@@ -1,0 +1,68 @@
+"""Frame sharding across ranks (one process per GPU; torch.distributed for the plumbing).
+
+Every frame and pixel is independent; the only cross-frame dependency of a
+time-lapse stack is the reference phase φ_ref.  Each rank holds a stack of
+T frames: local frame 0 is the global reference frame, local frames 1..T−1 are the global
+flow frames r·(T−1)+1 … (r+1)·(T−1).  Two reference modes:
+
+* "recompute" (default): every rank demodulates the reference frame itself.  The kernel is
+  deterministic, so φ_ref is bitwise identical on all ranks, and it costs exactly what
+  waiting for rank 0's result would — no collective on the data path.
+* "broadcast": rank 0 demodulates the reference and NCCL-broadcasts φ_ref (4·H·W bytes)
+  over NVLink; the others wait for it.  For streams whose reference frame lives on one
+  rank only.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def rank_frame_indices(rank: int, world: int, T: int) -> list[int]:
+    """Global frame indices of rank's local stack: [0] + its T−1 flow frames."""
+    if T < 2:
+        raise ValueError("a time-lapse stack needs a reference and at least one flow frame")
+    del world
+    return [0] + list(range(rank * (T - 1) + 1, (rank + 1) * (T - 1) + 1))
+
+
+def distinct_output_frames(world: int, T: int) -> int:
+    """Distinct output frames of the whole job: the reference plus every rank's flow frames."""
+    return world * (T - 1) + 1
+
+
+def is_dist() -> bool:
+    return dist.is_available() and dist.is_initialized()
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    if not is_dist() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sharded_stack_step(local_frames: torch.Tensor, demod, demod_raw, ref_mode: str = "recompute",
+                       ref_buf: torch.Tensor | None = None):
+    """One step on this rank's local stack (local frame 0 = global reference).
+
+    demod(frames, ref) -> phases;  demod_raw(frame) -> raw α of one frame.
+    Returns (phases [T,H,W], φ_ref [H,W])."""
+    rank = dist.get_rank() if is_dist() else 0
+    if ref_mode == "recompute" or not is_dist():
+        ref = demod_raw(local_frames[0])
+    elif ref_mode == "broadcast":
+        if rank == 0:
+            ref = demod_raw(local_frames[0])
+            if ref_buf is not None:
+                ref_buf.copy_(ref)
+                ref = ref_buf
+        else:
+            ref = ref_buf if ref_buf is not None else torch.empty(
+                local_frames.shape[-2:], dtype=torch.float32, device=local_frames.device)
+        dist.broadcast(ref, src=0)
+    else:
+        raise ValueError(ref_mode)
+    return demod(local_frames, ref), ref

@@ -100,8 +100,15 @@ class Workload:
         if self.kind == "diffusion":
             if t == 0:
                 return torch.zeros(H, W, dtype=torch.float64, device=device)
-            return phase_diffusion(H, W, self.times[t], device)
+            return phase_diffusion(H, W, self.time_of(t), device)
         raise ValueError(self.kind)
+
+    def time_of(self, t: int) -> float:
+        """Diffusion time of global flow frame t ≥ 1.  Frame indices beyond the schedule
+        (multi-GPU weak scaling: rank r owns flow frames r·(T−1)+1 … (r+1)·(T−1)) repeat the
+        schedule; their noise is still keyed by the global index."""
+        n = len(self.times) - 1
+        return self.times[(t - 1) % n + 1]
 
 
 def workload(name: str, **over) -> Workload:

@@ -1,0 +1,207 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the FP64 oracle on the same seeded
+complex64 bytes.  Tolerance (BASELINE north_star): RMS ≤ 1e-3 rad, max ≤ 1e-2 rad of the
+wrapped error over pixels the oracle does not flag (bits 0-4)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import rootmusic as R
+from paper_1910_11872_b200 import bosrm, synth
+
+from .parity_util import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+    bosrm.lib()
+
+
+def _interior(H, W, M):
+    b = int(math.ceil(M / 2))
+    m = np.zeros((H, W), bool)
+    m[b:H - b, b:W - b] = True
+    return m
+
+
+def run_gpu(frames_cpu, M, ref=None, flags=True):
+    f = frames_cpu.to(DEV)
+    r = None if ref is None else torch.as_tensor(ref, dtype=torch.float32).to(DEV)
+    out, fl = bosrm.bos_rootmusic_demod(f, M, ref_phase=r, flags=flags)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), (fl.cpu().numpy() if fl is not None else None)
+
+
+# ------------------------------------------------------------------------------- C1
+@pytest.mark.parametrize("M", [8, 9])
+def test_c1_full_frame_parity_and_closed_form(M):
+    w = synth.workload("C1")
+    f = synth.make_frame(w, 0)
+    g, gfl = run_gpu(f, M)
+    o, ofl = R.demod_frame(f.numpy(), M)
+    s = assert_parity(g, o, ofl, f"C1 M={M}", max_excluded_frac=0.0)
+    assert s["n"] == 256 * 256
+    truth = synth.true_phase(w, 0).numpy()
+    m = _interior(256, 256, M)
+    assert np.abs(R.wrap(g - truth))[m].max() <= 1e-3
+    assert np.all((gfl & bosrm.FLAG_BORDER) == (ofl & R.FLAG_BORDER))
+
+
+def test_c1_plane_variant():
+    w = synth.workload("C1plane")
+    f = synth.make_frame(w, 0)
+    g, _ = run_gpu(f, 8, flags=False)
+    o, ofl = R.demod_frame(f.numpy(), 8)
+    assert_parity(g, o, ofl, "C1plane", max_excluded_frac=0.0)
+
+
+# ------------------------------------------------------------------------------- C2
+@pytest.mark.parametrize("M,snr,full", [(11, 0.0, True), (8, 0.0, False), (11, 10.0, False),
+                                        (8, 20.0, False), (11, 5.0, False), (8, 15.0, False)])
+def test_c2_pair_parity(M, snr, full):
+    """512² reference + flow pair (carrier-only reference) through the stack entry point."""
+    w = synth.workload("C2")
+    stack = synth.make_stack(w, snr_db=snr)
+    out, fl, ref = bosrm.bos_rootmusic_demod_stack(stack.to(DEV), M, ref_index=0, flags=True)
+    torch.cuda.synchronize()
+    g = out.cpu().numpy()
+    assert np.all(g[0][np.isfinite(g[0])] == 0.0)
+    if full:
+        pix = None
+    else:
+        rng = np.random.default_rng(int(snr * 10) + M)
+        pix = (rng.integers(0, w.H, 16384), rng.integers(0, w.W, 16384))
+    o, ofl = R.demod_stack(stack.numpy(), M, pixels=pix, frame_indices=[1])
+    gg = g[1] if pix is None else g[1][pix]
+    assert_parity(gg, o[0], ofl[0], f"C2 M={M} snr={snr}")
+
+
+# ------------------------------------------------------------------- ragged / all M
+@pytest.mark.parametrize("M", list(range(3, 17)))
+def test_all_window_lengths_ragged_frame(M):
+    """Every instantiated M on a ragged 37×45 frame (not a multiple of the 32×4 tile)."""
+    w = synth.workload("C2", H=37, W=45, seed=M)
+    H, W = 37, 45
+    # smooth carrier fringe with mild phase, 10 dB
+    f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M), 5, snr_db=10.0)
+    g, gfl = run_gpu(f, M)
+    o, ofl = R.demod_frame(f.numpy(), M)
+    assert_parity(g, o, ofl, f"ragged M={M}", max_excluded_frac=0.05)
+    assert np.all((gfl & bosrm.FLAG_BORDER) == (ofl & R.FLAG_BORDER))
+    del w
+
+
+def test_minimum_frame_equals_window():
+    for M in (3, 8, 16):
+        f = synth.make_frame(synth.workload("C3", H=M, W=M, seed=2), 3, snr_db=20.0)
+        g, _ = run_gpu(f, M)
+        o, ofl = R.demod_frame(f.numpy(), M)
+        assert_parity(g, o, ofl, f"min M={M}", max_excluded_frac=0.2)
+
+
+def test_nonfinite_zero_and_constant_inputs():
+    H = W = 40
+    f = synth.make_frame(synth.workload("C1plane", H=H, W=W), 0).clone()
+    f[20, 20] = complex(float("nan"), 0.0)
+    g, gfl = run_gpu(f, 7)
+    assert np.isnan(g[20, 20]) and gfl[20, 20] & bosrm.FLAG_NONFINITE
+    assert np.isnan(g[17, 23]) and gfl[17, 23] & bosrm.FLAG_NONFINITE
+    assert np.isfinite(g[5, 5]) and not (gfl[5, 5] & bosrm.FLAG_NONFINITE)
+    z = torch.zeros(H, W, dtype=torch.complex64)
+    g, gfl = run_gpu(z, 7)
+    assert np.all(gfl & (bosrm.FLAG_LOW_AMPLITUDE | bosrm.FLAG_NONCONVERGED))
+    c = torch.full((H, W), complex(math.cos(1.0), math.sin(1.0)), dtype=torch.complex64)
+    g, gfl = run_gpu(c, 8)
+    assert np.max(np.abs(R.wrap(g - 1.0))) < 1e-4
+
+
+# ----------------------------------------------------------- stack / determinism / API
+def test_stack_determinism_and_shard_invariance():
+    w = synth.workload("C3", H=96, W=80)
+    stack = synth.make_stack(w, frames=range(6)).to(DEV)
+    a, fa, ra = bosrm.bos_rootmusic_demod_stack(stack, 8, ref_index=0, flags=True)
+    b, fb, rb = bosrm.bos_rootmusic_demod_stack(stack, 8, ref_index=0, flags=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(fa, fb)
+    # frame sharding: [0:2] and [2:6] against the same reference give the same bytes
+    s1, _ = bosrm.bos_rootmusic_demod(stack[0:2].contiguous(), 8, ref_phase=ra)
+    s2, _ = bosrm.bos_rootmusic_demod(stack[2:6].contiguous(), 8, ref_phase=ra)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([s1, s2]), a)
+    fin = torch.isfinite(a[0])
+    assert torch.all(a[0][fin] == 0)
+    # nonzero ref index
+    c, _, rc = bosrm.bos_rootmusic_demod_stack(stack, 8, ref_index=3)
+    torch.cuda.synchronize()
+    assert torch.all(c[3][torch.isfinite(c[3])] == 0)
+
+
+def test_host_api_matches_device_api():
+    w = synth.workload("C3", H=64, W=96)
+    stack = synth.make_stack(w, frames=range(7))
+    dev_out, dev_fl, _ = bosrm.bos_rootmusic_demod_stack(stack.to(DEV), 8, ref_index=0, flags=True)
+    h = stack.pin_memory()
+    h_out, h_fl = bosrm.bos_rootmusic_demod_stack_host(h, 8, ref_index=0, h_flags=True, chunk_frames=2)
+    torch.cuda.synchronize()
+    assert torch.equal(h_out, dev_out.cpu()) and torch.equal(h_fl, dev_fl.cpu())
+    # pageable host memory works too
+    h_out2, _ = bosrm.bos_rootmusic_demod_stack_host(stack.clone(), 8, ref_index=0, chunk_frames=3)
+    torch.cuda.synchronize()
+    assert torch.equal(h_out2, dev_out.cpu())
+
+
+def test_error_codes_on_device():
+    f = torch.zeros(1, 32, 32, dtype=torch.complex64, device=DEV)
+    out = torch.empty(1, 32, 32, dtype=torch.float32, device=DEV)
+    L = bosrm.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.bos_rootmusic_demod(f.data_ptr(), 1, 32, 32, 8, 2, None, out.data_ptr(), None, s) == \
+        bosrm.BOS_ERR_UNSUPPORTED
+    hostbuf = torch.zeros(1, 32, 32, dtype=torch.float32)
+    assert L.bos_rootmusic_demod(f.data_ptr(), 1, 32, 32, 8, 3, None, hostbuf.data_ptr(), None, s) == \
+        bosrm.BOS_ERR_INVALID_ARG
+    assert L.bos_rootmusic_demod(f.data_ptr(), 1, 32, 32, 8, 3, None, f.data_ptr(), None, s) == \
+        bosrm.BOS_ERR_INVALID_ARG
+    assert L.bos_rootmusic_demod(f.data_ptr(), 1, 32, 32, 17, 3, None, out.data_ptr(), None, s) == \
+        bosrm.BOS_ERR_UNSUPPORTED
+    with pytest.raises(bosrm.BosError):
+        bosrm.bos_rootmusic_demod(f, 2)
+
+
+def test_iteration_counts_variant_matches():
+    w = synth.workload("C3", H=64, W=64)
+    f = synth.make_stack(w, frames=[4]).to(DEV)
+    a, _ = bosrm.bos_rootmusic_demod(f, 8)
+    c = bosrm.bos_rootmusic_iteration_counts(f, 8)
+    torch.cuda.synchronize()
+    assert c["pixels"] == 64 * 64
+    assert torch.equal(a, c["out"])
+    assert 1 <= c["power_its"] / c["pixels"] <= 64
+    assert 1 <= c["aberth_y"] / c["pixels"] <= 40
+
+
+# ------------------------------------------------------------------- C3 at full size
+def test_c3_full_size_sampled_parity():
+    """1024²×100 diffusion stack, the bench configuration (one stack call, M=8); sampled
+    pixels of frames {1, 50, 99} against the oracle on the same bytes."""
+    w = synth.workload("C3")
+    stack = synth.make_stack(w, device=DEV)
+    out, fl, ref = bosrm.bos_rootmusic_demod_stack(stack, 8, ref_index=0, flags=True)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(11)
+    pix = (rng.integers(0, w.H, 4096), rng.integers(0, w.W, 4096))
+    frames = [0, 1, 50, 99]
+    host = stack[frames].cpu().numpy()
+    o, ofl = R.demod_stack(host, 8, ref_index=0, pixels=pix, frame_indices=[1, 2, 3])
+    g = out[[1, 50, 99]].cpu().numpy()
+    for j in range(3):
+        assert_parity(g[j][pix], o[j], ofl[j], f"C3 frame {frames[j + 1]}")
