@@ -82,6 +82,16 @@ __device__ __forceinline__ constexpr int tri_off(int i, int j) {  // strict lowe
 
 // Roots of P(z) = Σ_{n=0}^{N} c_n z^n (N = 2M−2) by Gauss–Seidel Aberth–Ehrlich iteration.
 // Returns the number of sweeps; `ok` = converged (tolerance) or stagnated at FP32 noise.
+//
+// Code size: the sweep over roots is a rolled loop that always updates z[0] and then
+// rotates the array by one (after N steps it is back in order, and root i has seen the
+// already-updated roots 0..i−1 — Gauss–Seidel).  All register indices stay static, and the
+// I-cache holds one root update instead of N unrolled copies.
+//
+// P is conjugate-palindromic (c_{N−k} = conj(c_k), Eqs.(12)-(13) with Hermitian C), so for
+// |z| > 1 the Newton ratio is evaluated through the reversed polynomial
+// Q(u) = z^{−N}P(z) = conj(P(conj u)), u = 1/z:  P/P′ = z·Q/(N·Q − u·Q′).  Horner then always
+// runs at |v| ≤ 1 (v = z or 1/z̄): no overflow for far roots, better relative accuracy.
 template <int N>
 __device__ __forceinline__ int aberth(const float2 (&c)[N + 1], float2 (&z)[N], bool& ok) {
     float prev = CUDART_INF_F;
@@ -89,28 +99,47 @@ __device__ __forceinline__ int aberth(const float2 (&c)[N + 1], float2 (&z)[N], 
     ok = false;
     for (; it < kAberthMaxIt; ++it) {
         float maxw = 0.0f;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-            const float2 zi = z[i];
+#pragma unroll 1
+        for (int r = 0; r < N; ++r) {
+            const float2 zi = z[0];
+            const float m2 = cabs2(zi);
+            const bool outside = m2 > 1.0f;
+            const float inv_m2 = __fdividef(1.0f, m2);
+            const float2 v = outside ? cscale(zi, inv_m2) : zi;        // 1/z̄ or z
             float2 p = c[N];
             float2 dp = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int k = N - 1; k >= 0; --k) {
-                dp = cfma(dp, zi, p);
-                p = cfma(p, zi, c[k]);
+                dp = cfma(dp, v, p);
+                p = cfma(p, v, c[k]);
             }
-            const float2 ratio = cdiv(p, dp);          // Newton step P/P'
+            float2 num, den;
+            if (outside) {
+                // Q = conj(P(v)), Q′ = conj(P′(v)), u = 1/z = conj(v):  ratio = z·Q / (N·Q − u·Q′)
+                const float2 q = cconj(p), dq = cconj(dp), u = cconj(v);
+                num = cmul(zi, q);
+                den = csub(cscale(q, float(N)), cmul(u, dq));
+            } else {
+                num = p;
+                den = dp;
+            }
+            const float2 ratio = cdiv(num, den);                    // Newton step P/P′
             float2 s = make_float2(0.0f, 0.0f);
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                if (j != i) s = cadd(s, crcp(csub(zi, z[j])));
+            for (int j = 1; j < N; ++j) s = cadd(s, crcp(csub(zi, z[j])));
+            // Aberth correction w = ratio / (1 − ratio·s)
+            const float2 d1 = make_float2(1.0f - (ratio.x * s.x - ratio.y * s.y), -(ratio.x * s.y + ratio.y * s.x));
+            float2 w = cdiv(ratio, d1);
+            float w2 = cabs2(w);
+            if (!(w2 < 1e30f)) {            // degenerate step (P′ = 0 or 1 = ratio·s): skip
+                w = make_float2(0.0f, 0.0f);
+                w2 = 0.0f;
             }
-            // w = ratio / (1 − ratio·s)
-            const float2 den = make_float2(1.0f - (ratio.x * s.x - ratio.y * s.y),
-                                           -(ratio.x * s.y + ratio.y * s.x));
-            const float2 w = cdiv(ratio, den);
-            z[i] = csub(zi, w);
-            maxw = fmaxf(maxw, cabs2(w));
+            const float2 zn = csub(zi, w);
+            maxw = fmaxf(maxw, w2);
+#pragma unroll
+            for (int j = 0; j + 1 < N; ++j) z[j] = z[j + 1];
+            z[N - 1] = zn;
         }
         if (maxw < kAberthTol2) { ok = true; ++it; break; }
         // Multiple (noise-free, double) roots converge linearly down to the FP32 noise
@@ -174,8 +203,14 @@ __device__ __forceinline__ float2 music_coeffs(const float2 (&q)[M], float2 (&c)
     return make_float2(r1.x * inv, -r1.y * inv);
 }
 
+// CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).
+template <int M>
+constexpr int min_blocks_per_sm() {
+    return M <= 8 ? 4 : (M <= 10 ? 3 : (M <= 13 ? 2 : 1));
+}
+
 template <int M, bool COUNT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, min_blocks_per_sm<M>())
 demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
              const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
              unsigned long long* __restrict__ counters) {
@@ -215,8 +250,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
             for (int i = 0; i < M; ++i) Rd[i] = 0.0f;
 #pragma unroll
             for (int t = 0; t < NOFF; ++t) Ro[t] = make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int k = 0; k < M; ++k) {
+#pragma unroll 1
+            for (int k = 0; k < M; ++k) {   // rolled: one column of Γ_w per trip (code size, regs)
                 float2 col[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) col[i] = win[i * TW + k];
@@ -278,38 +313,41 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 float2 v[M];
                 float vn = 0.0f;
 #pragma unroll
-                for (int k = 0; k < M; ++k) {
-                    float2 acc = make_float2(0.0f, 0.0f);
+                for (int k = 0; k < M; ++k) v[k] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+                for (int i = 0; i < M; ++i) {     // rolled over rows: v += conj(Γ_w(i,:)) u_i
+                    float2 ui = u[0];
 #pragma unroll
-                    for (int i = 0; i < M; ++i) acc = cfmac(u[i], win[i * TW + k], acc);  // u_i conj(Γ)
-                    v[k] = acc;
-                    vn += cabs2(acc);
+                    for (int t = 1; t < M; ++t) ui = (t == i) ? u[t] : ui;
+#pragma unroll
+                    for (int k = 0; k < M; ++k) v[k] = cfmac(ui, win[i * TW + k], v[k]);  // u_i conj(Γ)
                 }
+#pragma unroll
+                for (int k = 0; k < M; ++k) vn += cabs2(v[k]);
                 const float vinv = rsqrtf(vn);
 #pragma unroll
                 for (int k = 0; k < M; ++k) v[k] = cscale(v[k], vinv);
 
-                // ---- a4 + a5, y axis then x axis ----
-                float2 zy, zx;
-                float my, mx;
-                bool aby_ok, abx_ok;
-                {
+                // ---- a4 + a5, y axis (u_1) then x axis (v_1), one rolled loop ----
+                float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
+                float my = CUDART_INF_F, mx = CUDART_INF_F;
+                bool aby_ok = false, abx_ok = false;
+#pragma unroll 1
+                for (int axis = 0; axis < 2; ++axis) {
+                    float2 q[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : u[i];
                     float2 c[N + 1];
-                    const float2 rot = music_coeffs<M>(u, c);
+                    const float2 rot = music_coeffs<M>(q, c);
                     float2 z[N];
 #pragma unroll
                     for (int j = 0; j < N; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
-                    n_aby = aberth<N>(c, z, aby_ok);
-                    zy = select_root<N>(z, my);
-                }
-                {
-                    float2 c[N + 1];
-                    const float2 rot = music_coeffs<M>(v, c);
-                    float2 z[N];
-#pragma unroll
-                    for (int j = 0; j < N; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
-                    n_abx = aberth<N>(c, z, abx_ok);
-                    zx = select_root<N>(z, mx);
+                    bool ok;
+                    const int its = aberth<N>(c, z, ok);
+                    float marg;
+                    const float2 zs = select_root<N>(z, marg);
+                    if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
+                    else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }
                 }
                 if (!pow_ok || !aby_ok || !abx_ok || !isfinite(zy.x + zy.y + zx.x + zx.y))
                     fl |= kFlagNonconverged;
@@ -332,7 +370,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
 #pragma unroll
                 for (int i = 0; i < O0; ++i) q = cmul(q, hy);
                 float2 csum = make_float2(0.0f, 0.0f);
-#pragma unroll
+#pragma unroll 1
                 for (int i = 0; i < M; ++i) {
                     float2 row = make_float2(0.0f, 0.0f);
 #pragma unroll

@@ -34,11 +34,13 @@ def _interior(H, W, M):
 
 
 def run_gpu(frames_cpu, M, ref=None, flags=True):
+    """[H,W] (or [T,H,W]) CPU frames → GPU phase/flags with the same shape."""
     f = frames_cpu.to(DEV)
     r = None if ref is None else torch.as_tensor(ref, dtype=torch.float32).to(DEV)
     out, fl = bosrm.bos_rootmusic_demod(f, M, ref_phase=r, flags=flags)
     torch.cuda.synchronize()
-    return out.cpu().numpy(), (fl.cpu().numpy() if fl is not None else None)
+    shape = tuple(frames_cpu.shape)
+    return out.cpu().numpy().reshape(shape), (fl.cpu().numpy().reshape(shape) if fl is not None else None)
 
 
 # ------------------------------------------------------------------------------- C1
