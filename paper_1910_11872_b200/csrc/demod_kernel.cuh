@@ -80,66 +80,80 @@ __device__ __forceinline__ constexpr int tri_off(int i, int j) {  // strict lowe
     return i * (i - 1) / 2 + j;
 }
 
-// Roots of P(z) = Σ_{n=0}^{N} c_n z^n (N = 2M−2) by Gauss–Seidel Aberth–Ehrlich iteration.
-// Returns the number of sweeps; `ok` = converged (tolerance) or stagnated at FP32 noise.
-//
-// Code size: the sweep over roots is a rolled loop that always updates z[0] and then
-// rotates the array by one (after N steps it is back in order, and root i has seen the
-// already-updated roots 0..i−1 — Gauss–Seidel).  All register indices stay static, and the
-// I-cache holds one root update instead of N unrolled copies.
-//
-// P is conjugate-palindromic (c_{N−k} = conj(c_k), Eqs.(12)-(13) with Hermitian C), so for
-// |z| > 1 the Newton ratio is evaluated through the reversed polynomial
-// Q(u) = z^{−N}P(z) = conj(P(conj u)), u = 1/z:  P/P′ = z·Q/(N·Q − u·Q′).  Horner then always
+// Newton ratio P(z)/P′(z) of the conjugate-palindromic P (c_{N−k} = conj(c_k): C is
+// Hermitian in Eqs.(12)-(13)).  For |z| > 1 it goes through the reversed polynomial
+// Q(u) = z^{−N}P(z) = conj(P(conj u)), u = 1/z:  P/P′ = z·Q/(N·Q − u·Q′), so Horner always
 // runs at |v| ≤ 1 (v = z or 1/z̄): no overflow for far roots, better relative accuracy.
 template <int N>
-__device__ __forceinline__ int aberth(const float2 (&c)[N + 1], float2 (&z)[N], bool& ok) {
+__device__ __forceinline__ float2 newton_ratio(const float2 (&c)[N + 1], float2 zi) {
+    const float m2 = cabs2(zi);
+    const bool outside = m2 > 1.0f;
+    const float2 v = outside ? cscale(zi, __fdividef(1.0f, m2)) : zi;   // 1/z̄ or z
+    float2 p = c[N];
+    float2 dp = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+        dp = cfma(dp, v, p);
+        p = cfma(p, v, c[k]);
+    }
+    float2 num = p, den = dp;
+    if (outside) {
+        const float2 q = cconj(p), dq = cconj(dp), u = cconj(v);
+        num = cmul(zi, q);
+        den = csub(cscale(q, float(N)), cmul(u, dq));
+    }
+    return cdiv(num, den);
+}
+
+// All roots of P (degree N = 2M−2) by a Gauss–Seidel Aberth–Ehrlich iteration that tracks
+// only K = N/2 roots z_k and uses their mirrors 1/z̄_k for the other half.  On the unit circle
+// P(e^{jθ})e^{−j(M−1)θ} = u^H(θ) C u(θ) ≥ 0 (C = U_nU_n^H is PSD), so roots on the circle have
+// even multiplicity and the root multiset is exactly {z_k, 1/z̄_k} (Fejér–Riesz): the
+// symmetric iteration finds the same root set as the companion matrix for half the
+// Horner evaluations and half the reciprocal sums.
+//
+// Code size: the sweep over roots is a rolled loop that always updates z[0] and then
+// rotates the arrays by one (after K steps they are back in order, and root k has seen the
+// already-updated roots 0..k−1).  All register indices stay static; the I-cache holds one
+// root update.  Returns the number of sweeps; `ok` = converged or stagnated at FP32 noise.
+template <int N>
+__device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[N / 2], bool& ok) {
+    constexpr int K = N / 2;
+    float2 zm[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) zm[k] = cscale(z[k], __fdividef(1.0f, cabs2(z[k])));
     float prev = CUDART_INF_F;
     int it = 0;
     ok = false;
     for (; it < kAberthMaxIt; ++it) {
         float maxw = 0.0f;
 #pragma unroll 1
-        for (int r = 0; r < N; ++r) {
+        for (int r = 0; r < K; ++r) {
             const float2 zi = z[0];
-            const float m2 = cabs2(zi);
-            const bool outside = m2 > 1.0f;
-            const float inv_m2 = __fdividef(1.0f, m2);
-            const float2 v = outside ? cscale(zi, inv_m2) : zi;        // 1/z̄ or z
-            float2 p = c[N];
-            float2 dp = make_float2(0.0f, 0.0f);
+            const float2 ratio = newton_ratio<N>(c, zi);
+            float2 s = crcp(csub(zi, zm[0]));
 #pragma unroll
-            for (int k = N - 1; k >= 0; --k) {
-                dp = cfma(dp, v, p);
-                p = cfma(p, v, c[k]);
+            for (int j = 1; j < K; ++j) {
+                s = cadd(s, crcp(csub(zi, z[j])));
+                s = cadd(s, crcp(csub(zi, zm[j])));
             }
-            float2 num, den;
-            if (outside) {
-                // Q = conj(P(v)), Q′ = conj(P′(v)), u = 1/z = conj(v):  ratio = z·Q / (N·Q − u·Q′)
-                const float2 q = cconj(p), dq = cconj(dp), u = cconj(v);
-                num = cmul(zi, q);
-                den = csub(cscale(q, float(N)), cmul(u, dq));
-            } else {
-                num = p;
-                den = dp;
-            }
-            const float2 ratio = cdiv(num, den);                    // Newton step P/P′
-            float2 s = make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int j = 1; j < N; ++j) s = cadd(s, crcp(csub(zi, z[j])));
             // Aberth correction w = ratio / (1 − ratio·s)
             const float2 d1 = make_float2(1.0f - (ratio.x * s.x - ratio.y * s.y), -(ratio.x * s.y + ratio.y * s.x));
             float2 w = cdiv(ratio, d1);
             float w2 = cabs2(w);
-            if (!(w2 < 1e30f)) {            // degenerate step (P′ = 0 or 1 = ratio·s): skip
+            if (!(w2 < 1e30f)) {            // degenerate step (P′ = 0 or ratio·s = 1): skip
                 w = make_float2(0.0f, 0.0f);
                 w2 = 0.0f;
             }
             const float2 zn = csub(zi, w);
             maxw = fmaxf(maxw, w2);
 #pragma unroll
-            for (int j = 0; j + 1 < N; ++j) z[j] = z[j + 1];
-            z[N - 1] = zn;
+            for (int j = 0; j + 1 < K; ++j) {
+                z[j] = z[j + 1];
+                zm[j] = zm[j + 1];
+            }
+            z[K - 1] = zn;
+            zm[K - 1] = cscale(zn, __fdividef(1.0f, cabs2(zn)));
         }
         if (maxw < kAberthTol2) { ok = true; ++it; break; }
         // Multiple (noise-free, double) roots converge linearly down to the FP32 noise
@@ -151,13 +165,14 @@ __device__ __forceinline__ int aberth(const float2 (&c)[N + 1], float2 (&z)[N], 
 }
 
 // Root closest to the unit circle (min |ln|z||, via the monotone tanh(|ln r|) =
-// |r²−1|/(r²+1)) and the margin to the best root of a different frequency.
-template <int N>
-__device__ __forceinline__ float2 select_root(const float2 (&z)[N], float& margin) {
+// |r²−1|/(r²+1); a root and its mirror tie) and the margin to the best root of a
+// different frequency.
+template <int K>
+__device__ __forceinline__ float2 select_root(const float2 (&z)[K], float& margin) {
     float best = CUDART_INF_F;
     float2 zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+    for (int i = 0; i < K; ++i) {
         const float r2 = cabs2(z[i]);
         const float d = fabsf(r2 - 1.0f) / (r2 + 1.0f);
         if (d < best) { best = d; zb = z[i]; }
@@ -165,7 +180,7 @@ __device__ __forceinline__ float2 select_root(const float2 (&z)[N], float& margi
     const float rb = sqrtf(cabs2(zb));
     float second = CUDART_INF_F;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+    for (int i = 0; i < K; ++i) {
         const float r2 = cabs2(z[i]);
         const float d = fabsf(r2 - 1.0f) / (r2 + 1.0f);
         const float dot = fmaf(z[i].x, zb.x, z[i].y * zb.y);        // Re(z_i conj(z_b))
@@ -339,13 +354,13 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : u[i];
                     float2 c[N + 1];
                     const float2 rot = music_coeffs<M>(q, c);
-                    float2 z[N];
+                    float2 z[N / 2];    // the inside half of the rotated template
 #pragma unroll
-                    for (int j = 0; j < N; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
+                    for (int j = 0; j < N / 2; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
                     bool ok;
-                    const int its = aberth<N>(c, z, ok);
+                    const int its = aberth_sym<N>(c, z, ok);
                     float marg;
-                    const float2 zs = select_root<N>(z, marg);
+                    const float2 zs = select_root<N / 2>(z, marg);
                     if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
                     else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }
                 }
