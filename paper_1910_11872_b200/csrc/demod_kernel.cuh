@@ -35,6 +35,7 @@ constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyon
 constexpr float kPowerTol = 4e-13f;   // ‖u_{k+1} − u_k‖² stop
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 constexpr float kAberthTol2 = 1e-12f; // max_i |Δz_i|² stop
+constexpr float kNearCircle = 2e-3f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCosTauOmega = 0.99995000042f;  // cos(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
 constexpr float kLowAmp = 1e-4f;      // LOW_AMPLITUDE threshold
@@ -131,7 +132,12 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
         for (int r = 0; r < K; ++r) {
             const float2 zi = z[0];
             const float2 ratio = newton_ratio<N>(c, zi);
-            float2 s = crcp(csub(zi, zm[0]));
+            // Own-mirror term.  Near the unit circle z and 1/z̄ merge into one (near-)double
+            // root; keeping the term there freezes the tangential (arg = ω) error, so the
+            // update falls back to a plain Newton/Aberth step on the cluster (linear, ratio
+            // 1/2, for an exact double root; quadratic once inside a split pair).
+            const bool near = fabsf(1.0f - cabs2(zi)) < kNearCircle;
+            float2 s = near ? make_float2(0.0f, 0.0f) : crcp(csub(zi, zm[0]));
 #pragma unroll
             for (int j = 1; j < K; ++j) {
                 s = cadd(s, crcp(csub(zi, z[j])));
