@@ -35,7 +35,7 @@ constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyon
 constexpr float kPowerTol = 4e-13f;   // ‖u_{k+1} − u_k‖² stop
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 constexpr float kAberthTol2 = 1e-12f; // max_i |Δz_i|² stop
-constexpr float kNearCircle = 2e-3f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
+constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCosTauOmega = 0.99995000042f;  // cos(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
 constexpr float kLowAmp = 1e-4f;      // LOW_AMPLITUDE threshold
@@ -106,6 +106,21 @@ __device__ __forceinline__ float2 newton_ratio(const float2 (&c)[N + 1], float2 
     return cdiv(num, den);
 }
 
+// P′(z)/P″(z): the Newton step for P′ (used for near-double roots on the unit circle).
+// Horner with three accumulators: dp = P′(z), ddp = P″(z)/2.
+template <int N>
+__device__ __forceinline__ float2 newton_on_derivative(const float2 (&c)[N + 1], float2 z) {
+    float2 p = c[N];
+    float2 dp = make_float2(0.0f, 0.0f), ddp = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+        ddp = cfma(ddp, z, dp);
+        dp = cfma(dp, z, p);
+        p = cfma(p, z, c[k]);
+    }
+    return cdiv(dp, cscale(ddp, 2.0f));
+}
+
 // All roots of P (degree N = 2M−2) by a Gauss–Seidel Aberth–Ehrlich iteration that tracks
 // only K = N/2 roots z_k and uses their mirrors 1/z̄_k for the other half.  On the unit circle
 // P(e^{jθ})e^{−j(M−1)θ} = u^H(θ) C u(θ) ≥ 0 (C = U_nU_n^H is PSD), so roots on the circle have
@@ -133,9 +148,10 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
             const float2 zi = z[0];
             const float2 ratio = newton_ratio<N>(c, zi);
             // Own-mirror term.  Near the unit circle z and 1/z̄ merge into one (near-)double
-            // root; keeping the term there freezes the tangential (arg = ω) error, so the
-            // update falls back to a plain Newton/Aberth step on the cluster (linear, ratio
-            // 1/2, for an exact double root; quadratic once inside a split pair).
+            // root: keeping the term there freezes the tangential (arg = ω) error.  There the
+            // update is Newton on P′ instead (a double root of P is a simple root of P′;
+            // quadratic), which lands on the pair's centre: same arg as the pair up to
+            // O(η²) for a pair split by η ≤ kNearCircle/2.
             const bool near = fabsf(1.0f - cabs2(zi)) < kNearCircle;
             float2 s = near ? make_float2(0.0f, 0.0f) : crcp(csub(zi, zm[0]));
 #pragma unroll
@@ -146,6 +162,7 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
             // Aberth correction w = ratio / (1 − ratio·s)
             const float2 d1 = make_float2(1.0f - (ratio.x * s.x - ratio.y * s.y), -(ratio.x * s.y + ratio.y * s.x));
             float2 w = cdiv(ratio, d1);
+            if (near) w = newton_on_derivative<N>(c, zi);
             float w2 = cabs2(w);
             if (!(w2 < 1e30f)) {            // degenerate step (P′ = 0 or ratio·s = 1): skip
                 w = make_float2(0.0f, 0.0f);

@@ -207,3 +207,15 @@ def test_c3_full_size_sampled_parity():
     g = out[[1, 50, 99]].cpu().numpy()
     for j in range(3):
         assert_parity(g[j][pix], o[j], ofl[j], f"C3 frame {frames[j + 1]}")
+
+
+@pytest.mark.parametrize("M", [4, 5, 8, 11, 16])
+@pytest.mark.parametrize("snr", [None, 40.0, 25.0])
+def test_high_snr_and_noise_free_parity(M, snr):
+    """Near-double roots on the unit circle (noise-free / high SNR) on a 64×72 crop-sized
+    frame of the C1 phantom: the regime where the signal root pair merges."""
+    w = synth.workload("C1", H=64, W=72)
+    f = synth.make_frame(w, 0, snr_db=snr)
+    g, _ = run_gpu(f, M)
+    o, ofl = R.demod_frame(f.numpy(), M)
+    assert_parity(g, o, ofl, f"high-SNR M={M} snr={snr}", max_excluded_frac=0.02)
