@@ -23,6 +23,7 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include "cx2.cuh"
 #include "template_roots.h"
 
 namespace bos {
@@ -86,20 +87,24 @@ __device__ __forceinline__ constexpr int tri_off(int i, int j) {  // strict lowe
 // Q(u) = z^{−N}P(z) = conj(P(conj u)), u = 1/z:  P/P′ = z·Q/(N·Q − u·Q′), so Horner always
 // runs at |v| ≤ 1 (v = z or 1/z̄): no overflow for far roots, better relative accuracy.
 template <int N>
-__device__ __forceinline__ float2 newton_ratio(const float2 (&c)[N + 1], float2 zi) {
+__device__ __forceinline__ float2 newton_ratio(const cx2 (&c)[N + 1], float2 zi) {
     const float m2 = cabs2(zi);
     const bool outside = m2 > 1.0f;
     const float2 v = outside ? cscale(zi, __fdividef(1.0f, m2)) : zi;   // 1/z̄ or z
-    float2 p = c[N];
-    float2 dp = make_float2(0.0f, 0.0f);
+    // V and j·V as genuine 64-bit values (an f32x2 op result), so the register allocator keeps
+    // each in one aligned pair instead of re-pairing scalars before every FFMA2.
+    const cx2 V = cx2_make(v.x, v.y);
+    const cx2 Vj = mul2(cx2_make(v.y, v.x), cx2_make(-1.0f, 1.0f));
+    cx2 p = c[N];
+    cx2 dp = 0ull;
 #pragma unroll
     for (int k = N - 1; k >= 0; --k) {
-        dp = cfma(dp, v, p);
-        p = cfma(p, v, c[k]);
+        dp = cmad2(dp, V, Vj, p);
+        p = cmad2(p, V, Vj, c[k]);
     }
-    float2 num = p, den = dp;
+    float2 num = cx2_f2(p), den = cx2_f2(dp);
     if (outside) {
-        const float2 q = cconj(p), dq = cconj(dp), u = cconj(v);
+        const float2 q = cconj(num), dq = cconj(den), u = cconj(v);
         num = cmul(zi, q);
         den = csub(cscale(q, float(N)), cmul(u, dq));
     }
@@ -109,16 +114,24 @@ __device__ __forceinline__ float2 newton_ratio(const float2 (&c)[N + 1], float2 
 // P′(z)/P″(z): the Newton step for P′ (used for near-double roots on the unit circle).
 // Horner with three accumulators: dp = P′(z), ddp = P″(z)/2.
 template <int N>
-__device__ __forceinline__ float2 newton_on_derivative(const float2 (&c)[N + 1], float2 z) {
-    float2 p = c[N];
-    float2 dp = make_float2(0.0f, 0.0f), ddp = make_float2(0.0f, 0.0f);
+__device__ __forceinline__ float2 newton_on_derivative(const cx2 (&c)[N + 1], float2 z) {
+    const cx2 V = cx2_make(z.x, z.y);
+    const cx2 Vj = mul2(cx2_make(z.y, z.x), cx2_make(-1.0f, 1.0f));
+    cx2 p = c[N];
+    cx2 dp = 0ull, ddp = 0ull;
 #pragma unroll
     for (int k = N - 1; k >= 0; --k) {
-        ddp = cfma(ddp, z, dp);
-        dp = cfma(dp, z, p);
-        p = cfma(p, z, c[k]);
+        ddp = cmad2(ddp, V, Vj, dp);
+        dp = cmad2(dp, V, Vj, p);
+        p = cmad2(p, V, Vj, c[k]);
     }
-    return cdiv(dp, cscale(ddp, 2.0f));
+    return cdiv(cx2_f2(dp), cscale(cx2_f2(ddp), 2.0f));
+}
+
+// 1/|z|² · z = 1/z̄ (the mirror of z through the unit circle)
+__device__ __forceinline__ cx2 mirror(cx2 z) {
+    const float re = cx2_re(z), im = cx2_im(z);
+    return mul2(z, cx2_bcast(rcp_approx(fmaf(re, re, im * im))));
 }
 
 // All roots of P (degree N = 2M−2) by a Gauss–Seidel Aberth–Ehrlich iteration that tracks
@@ -131,13 +144,15 @@ __device__ __forceinline__ float2 newton_on_derivative(const float2 (&c)[N + 1],
 // Code size: the sweep over roots is a rolled loop that always updates z[0] and then
 // rotates the arrays by one (after K steps they are back in order, and root k has seen the
 // already-updated roots 0..k−1).  All register indices stay static; the I-cache holds one
-// root update.  Returns the number of sweeps; `ok` = converged or stagnated at FP32 noise.
+// root update.  Complex values are packed (cx2.cuh): Horner and the reciprocal sum run on
+// FFMA2.  Returns the number of sweeps; `ok` = converged or stagnated at FP32 noise.
 template <int N>
-__device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[N / 2], bool& ok) {
+__device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2], bool& ok) {
     constexpr int K = N / 2;
-    float2 zm[K];
+    cx2 zm[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) zm[k] = cscale(z[k], __fdividef(1.0f, cabs2(z[k])));
+    for (int k = 0; k < K; ++k) zm[k] = mirror(z[k]);
+    const cx2 kNegPos = cx2_make(-1.0f, 1.0f);
     float prev = CUDART_INF_F;
     int it = 0;
     ok = false;
@@ -145,7 +160,7 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
         float maxw = 0.0f;
 #pragma unroll 1
         for (int r = 0; r < K; ++r) {
-            const float2 zi = z[0];
+            const float2 zi = cx2_f2(z[0]);
             const float2 ratio = newton_ratio<N>(c, zi);
             // Own-mirror term.  Near the unit circle z and 1/z̄ merge into one (near-)double
             // root: keeping the term there freezes the tangential (arg = ω) error.  There the
@@ -153,14 +168,27 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
             // quadratic), which lands on the pair's centre: same arg as the pair up to
             // O(η²) for a pair split by η ≤ kNearCircle/2.
             const bool near = fabsf(1.0f - cabs2(zi)) < kNearCircle;
-            float2 s = near ? make_float2(0.0f, 0.0f) : crcp(csub(zi, zm[0]));
+            // s = Σ 1/(z_i − z_j) = Σ conj(d)/|d|², d = z_i − z_j; conj(d) = conj(z_i) + (−1,1)⊙z_j
+            const cx2 ziC = mul2(z[0], cx2_make(1.0f, -1.0f));
+            cx2 s = 0ull;
+            {
+                const cx2 dc = fma2(zm[0], kNegPos, ziC);
+                const float q = fmaf(cx2_re(dc), cx2_re(dc), cx2_im(dc) * cx2_im(dc));
+                s = near ? 0ull : mul2(cx2_bcast(rcp_approx(q)), dc);
+            }
 #pragma unroll
             for (int j = 1; j < K; ++j) {
-                s = cadd(s, crcp(csub(zi, z[j])));
-                s = cadd(s, crcp(csub(zi, zm[j])));
+                const cx2 d1 = fma2(z[j], kNegPos, ziC);
+                const float q1 = fmaf(cx2_re(d1), cx2_re(d1), cx2_im(d1) * cx2_im(d1));
+                s = fma2(cx2_bcast(rcp_approx(q1)), d1, s);
+                const cx2 d2 = fma2(zm[j], kNegPos, ziC);
+                const float q2 = fmaf(cx2_re(d2), cx2_re(d2), cx2_im(d2) * cx2_im(d2));
+                s = fma2(cx2_bcast(rcp_approx(q2)), d2, s);
             }
+            const float2 sf = cx2_f2(s);
             // Aberth correction w = ratio / (1 − ratio·s)
-            const float2 d1 = make_float2(1.0f - (ratio.x * s.x - ratio.y * s.y), -(ratio.x * s.y + ratio.y * s.x));
+            const float2 d1 = make_float2(1.0f - (ratio.x * sf.x - ratio.y * sf.y),
+                                          -(ratio.x * sf.y + ratio.y * sf.x));
             float2 w = cdiv(ratio, d1);
             if (near) w = newton_on_derivative<N>(c, zi);
             float w2 = cabs2(w);
@@ -168,7 +196,7 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
                 w = make_float2(0.0f, 0.0f);
                 w2 = 0.0f;
             }
-            const float2 zn = csub(zi, w);
+            const cx2 zn = cx2_make(zi.x - w.x, zi.y - w.y);
             maxw = fmaxf(maxw, w2);
 #pragma unroll
             for (int j = 0; j + 1 < K; ++j) {
@@ -176,7 +204,7 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
                 zm[j] = zm[j + 1];
             }
             z[K - 1] = zn;
-            zm[K - 1] = cscale(zn, __fdividef(1.0f, cabs2(zn)));
+            zm[K - 1] = mirror(zn);
         }
         if (maxw < kAberthTol2) { ok = true; ++it; break; }
         // Multiple (noise-free, double) roots converge linearly down to the FP32 noise
@@ -191,7 +219,10 @@ __device__ __forceinline__ int aberth_sym(const float2 (&c)[N + 1], float2 (&z)[
 // |r²−1|/(r²+1); a root and its mirror tie) and the margin to the best root of a
 // different frequency.
 template <int K>
-__device__ __forceinline__ float2 select_root(const float2 (&z)[K], float& margin) {
+__device__ __forceinline__ float2 select_root(const cx2 (&zp)[K], float& margin) {
+    float2 z[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) z[i] = cx2_f2(zp[i]);
     float best = CUDART_INF_F;
     float2 zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
 #pragma unroll
@@ -220,19 +251,19 @@ __device__ __forceinline__ float2 select_root(const float2 (&z)[K], float& margi
 // c_{M−1} = M − ‖q‖², c_{M−1+d} = −r_d, c_{M−1−d} = −conj(r_d), r_d = Σ_i q_i conj(q_{i+d}).
 // Also returns the rotation e^{jω̂} = conj(r_1)/|r_1| (tone estimate for the template).
 template <int M>
-__device__ __forceinline__ float2 music_coeffs(const float2 (&q)[M], float2 (&c)[2 * M - 1]) {
+__device__ __forceinline__ float2 music_coeffs(const float2 (&q)[M], cx2 (&c)[2 * M - 1]) {
     float n2 = 0.0f;
 #pragma unroll
     for (int i = 0; i < M; ++i) n2 += cabs2(q[i]);
-    c[M - 1] = make_float2(float(M) - n2, 0.0f);
+    c[M - 1] = cx2_make(float(M) - n2, 0.0f);
     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int d = 1; d < M; ++d) {
         float2 r = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int i = 0; i + d < M; ++i) r = cfmac(q[i], q[i + d], r);
-        c[M - 1 + d] = make_float2(-r.x, -r.y);
-        c[M - 1 - d] = make_float2(-r.x, r.y);
+        c[M - 1 + d] = cx2_make(-r.x, -r.y);
+        c[M - 1 - d] = cx2_make(-r.x, r.y);
         if (d == 1) r1 = r;
     }
     const float n = cabs2(r1);
@@ -375,11 +406,11 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     float2 q[M];
 #pragma unroll
                     for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : u[i];
-                    float2 c[N + 1];
+                    cx2 c[N + 1];
                     const float2 rot = music_coeffs<M>(q, c);
-                    float2 z[N / 2];    // the inside half of the rotated template
+                    cx2 z[N / 2];       // the inside half of the rotated template
 #pragma unroll
-                    for (int j = 0; j < N / 2; ++j) z[j] = cmul(kTemplateRoots[bos_template_offset(M) + j], rot);
+                    for (int j = 0; j < N / 2; ++j) z[j] = f2_cx2(cmul(kTemplateRoots[bos_template_offset(M) + j], rot));
                     bool ok;
                     const int its = aberth_sym<N>(c, z, ok);
                     float marg;
