@@ -270,8 +270,16 @@ def run_cuda(args, world, rank, local):
     achieved = f_px * T * plane / (kern_ms / 1e3) / 1e12
     sm_max = float(P.get("sm_max_mhz", 1965.0))
     peak = B200_SMS * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        if int(tr.get("window_len", -1)) == M:
+            traffic = tr["dram_bytes_per_pixel"] * T * plane   # bytes per stack launch (ncu capture)
+    except (OSError, ValueError, KeyError):
+        traffic = None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "kernel": f"bos::demod_kernel<{M},false>", "kernel_ms": kern_ms,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/)", "kernel": f"bos::demod_kernel<{M},false>", "kernel_ms": kern_ms,
                 "kernel_share_of_step": kern_ms / ms_per_step,
                 "flops_per_px": f_px, "iters": {"power": k_pi, "aberth_y": k_aby, "aberth_x": k_abx},
                 "peak_basis": f"FP32 FMA: {B200_SMS} SM x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",
