@@ -35,7 +35,8 @@ constexpr int kThreads = kBX * kBY;
 constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyond)
 constexpr float kPowerTol = 4e-13f;   // ‖u_{k+1} − u_k‖² stop
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
-constexpr float kAberthTol2 = 1e-12f; // max_i |Δz_i|² stop
+constexpr float kAberthTol2 = 1e-6f;  // max_i |Δz_i|² stop (cubic convergence: the last
+                                      // update of ≤ 1e-3 leaves an error ~1e-9)
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCosTauOmega = 0.99995000042f;  // cos(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
@@ -313,22 +314,31 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 fl |= kFlagBorder;
 
             // ---- a2: R_y = Γ_w Γ_w^H, diagonal (real) + strict lower triangle ----
+            // R_ij += a·conj(b) (a = Γ(i,k), b = Γ(j,k)) = re(b)·a + im(b)·(−j·a): two FFMA2.
             float Rd[M];
-            float2 Ro[NOFF > 0 ? NOFF : 1];
+            cx2 Ro[NOFF > 0 ? NOFF : 1];
 #pragma unroll
             for (int i = 0; i < M; ++i) Rd[i] = 0.0f;
 #pragma unroll
-            for (int t = 0; t < NOFF; ++t) Ro[t] = make_float2(0.0f, 0.0f);
+            for (int t = 0; t < NOFF; ++t) Ro[t] = 0ull;
+            const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
 #pragma unroll 1
             for (int k = 0; k < M; ++k) {   // rolled: one column of Γ_w per trip (code size, regs)
-                float2 col[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) col[i] = win[i * TW + k];
+                cx2 col[M], colnj[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
-                    Rd[i] = fmaf(col[i].x, col[i].x, fmaf(col[i].y, col[i].y, Rd[i]));
+                    const float2 g = win[i * TW + k];
+                    col[i] = cx2_make(g.x, g.y);
+                    colnj[i] = mul2(cx2_make(g.y, g.x), kPosNeg);     // −j·a = (im a, −re a)
+                    Rd[i] = fmaf(g.x, g.x, fmaf(g.y, g.y, Rd[i]));
+                }
 #pragma unroll
-                    for (int j = 0; j < i; ++j) Ro[tri_off<M>(i, j)] = cfmac(col[i], col[j], Ro[tri_off<M>(i, j)]);
+                for (int i = 1; i < M; ++i) {
+#pragma unroll
+                    for (int j = 0; j < i; ++j) {
+                        cx2& r = Ro[tri_off<M>(i, j)];
+                        r = fma2(cx2_bcast(cx2_re(col[j])), col[i], fma2(cx2_bcast(cx2_im(col[j])), colnj[i], r));
+                    }
                 }
             }
             float trace = 0.0f;
@@ -345,57 +355,78 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 // start: u_i = e^{jω̂ i}/√M with e^{jω̂} ∝ Σ_i R[i+1][i] (lag-1 correlation)
                 float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, Ro[tri_off<M>(i + 1, i)]);
+                for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
                 float2 e = make_float2(1.0f, 0.0f);
                 if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
-                float2 u[M];
-                u[0] = make_float2(rsqrtf(float(M)), 0.0f);
-#pragma unroll
-                for (int i = 1; i < M; ++i) u[i] = cmul(u[i - 1], e);
-                bool pow_ok = false;
-                for (n_pow = 0; n_pow < kPowerMaxIt;) {
-                    float2 y[M];
+                cx2 u[M];
+                {
+                    float2 t = make_float2(rsqrtf(float(M)), 0.0f);
 #pragma unroll
                     for (int i = 0; i < M; ++i) {
-                        float2 acc = make_float2(Rd[i] * u[i].x, Rd[i] * u[i].y);
+                        u[i] = cx2_make(t.x, t.y);
+                        t = cmul(t, e);
+                    }
+                }
+                bool pow_ok = false;
+                for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                    // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
+                    cx2 uj[M];
 #pragma unroll
-                        for (int j = 0; j < i; ++j) acc = cfma(Ro[tri_off<M>(i, j)], u[j], acc);
+                    for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
+                    cx2 y[M];
 #pragma unroll
-                        for (int j = i + 1; j < M; ++j) acc = cfmac(u[j], Ro[tri_off<M>(j, i)], acc);
+                    for (int i = 0; i < M; ++i) {
+                        cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
+#pragma unroll
+                        for (int j = 0; j < i; ++j) {
+                            const cx2 r = Ro[tri_off<M>(i, j)];
+                            acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
+                        }
+#pragma unroll
+                        for (int j = i + 1; j < M; ++j) {
+                            const cx2 r = Ro[tri_off<M>(j, i)];
+                            acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
+                        }
                         y[i] = acc;
                     }
                     float nrm2 = 0.0f;
 #pragma unroll
-                    for (int i = 0; i < M; ++i) nrm2 += cabs2(y[i]);
-                    const float inv = rsqrtf(nrm2);
+                    for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+                    const cx2 inv = cx2_bcast(rsqrtf(nrm2));
                     float diff = 0.0f;
 #pragma unroll
                     for (int i = 0; i < M; ++i) {
-                        const float2 yn = cscale(y[i], inv);
-                        diff += cabs2(csub(yn, u[i]));
+                        const cx2 yn = mul2(y[i], inv);
+                        diff += cabs2(cx2_f2(sub2(yn, u[i])));
                         u[i] = yn;
                     }
                     ++n_pow;
                     if (diff < kPowerTol) { pow_ok = true; break; }
                 }
-                // v_1 ∝ Γ_w^H u_1
-                float2 v[M];
+                // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
+                cx2 unj[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) unj[i] = mul2(cx2_make(cx2_im(u[i]), cx2_re(u[i])), kPosNeg);
+                cx2 vp[M];
                 float vn = 0.0f;
 #pragma unroll
-                for (int k = 0; k < M; ++k) v[k] = make_float2(0.0f, 0.0f);
-#pragma unroll 1
-                for (int i = 0; i < M; ++i) {     // rolled over rows: v += conj(Γ_w(i,:)) u_i
-                    float2 ui = u[0];
+                for (int k = 0; k < M; ++k) {
+                    cx2 acc = 0ull;
 #pragma unroll
-                    for (int t = 1; t < M; ++t) ui = (t == i) ? u[t] : ui;
-#pragma unroll
-                    for (int k = 0; k < M; ++k) v[k] = cfmac(ui, win[i * TW + k], v[k]);  // u_i conj(Γ)
+                    for (int i = 0; i < M; ++i) {
+                        const float2 g = win[i * TW + k];
+                        acc = fma2(cx2_bcast(g.x), u[i], fma2(cx2_bcast(g.y), unj[i], acc));
+                    }
+                    vp[k] = acc;
+                    vn += cabs2(cx2_f2(acc));
                 }
+                const cx2 vinv = cx2_bcast(rsqrtf(vn));
+                float2 v[M];
 #pragma unroll
-                for (int k = 0; k < M; ++k) vn += cabs2(v[k]);
-                const float vinv = rsqrtf(vn);
+                for (int k = 0; k < M; ++k) v[k] = cx2_f2(mul2(vp[k], vinv));
+                float2 uf[M];
 #pragma unroll
-                for (int k = 0; k < M; ++k) v[k] = cscale(v[k], vinv);
+                for (int i = 0; i < M; ++i) uf[i] = cx2_f2(u[i]);
 
                 // ---- a4 + a5, y axis (u_1) then x axis (v_1), one rolled loop ----
                 float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
@@ -405,7 +436,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 for (int axis = 0; axis < 2; ++axis) {
                     float2 q[M];
 #pragma unroll
-                    for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : u[i];
+                    for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : uf[i];
                     cx2 c[N + 1];
                     const float2 rot = music_coeffs<M>(q, c);
                     cx2 z[N / 2];       // the inside half of the rotated template
@@ -426,14 +457,18 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 // ẑ_x = e^{-jω_x}, ẑ_y = e^{jω_y}; basis e^{-j(ω_x o_k + ω_y o_i)} = ẑ_x^{o_k} conj(ẑ_y)^{o_i}
                 const float2 hx = cscale(zx, rsqrtf(cabs2(zx)));
                 const float2 hy = cscale(zy, rsqrtf(cabs2(zy)));
-                float2 tw[M];
+                // row_i = Σ_k Γ(i,k)·tw_k = Σ_k re(g)·tw_k + im(g)·(j·tw_k)  (two FFMA2 per sample)
+                cx2 tw[M], twj[M];
                 {
                     float2 p = make_float2(1.0f, 0.0f);
 #pragma unroll
                     for (int k = 0; k < O0; ++k) p = cmul(p, cconj(hx));
-                    tw[0] = p;
 #pragma unroll
-                    for (int k = 1; k < M; ++k) tw[k] = cmul(tw[k - 1], hx);
+                    for (int k = 0; k < M; ++k) {
+                        tw[k] = cx2_make(p.x, p.y);
+                        twj[k] = cx2_make(-p.y, p.x);
+                        p = cmul(p, hx);
+                    }
                 }
                 float2 q = make_float2(1.0f, 0.0f);
 #pragma unroll
@@ -441,10 +476,13 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 float2 csum = make_float2(0.0f, 0.0f);
 #pragma unroll 1
                 for (int i = 0; i < M; ++i) {
-                    float2 row = make_float2(0.0f, 0.0f);
+                    cx2 row = 0ull;
 #pragma unroll
-                    for (int k = 0; k < M; ++k) row = cfma(win[i * TW + k], tw[k], row);
-                    csum = cfma(row, q, csum);
+                    for (int k = 0; k < M; ++k) {
+                        const float2 g = win[i * TW + k];
+                        row = fma2(cx2_bcast(g.x), tw[k], fma2(cx2_bcast(g.y), twj[k], row));
+                    }
+                    csum = cfma(cx2_f2(row), q, csum);
                     q = cmul(q, cconj(hy));
                 }
                 if (!(cabs2(csum) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
