@@ -67,11 +67,13 @@ def flops_per_pixel(M: int, k_pi: float, k_aby: float, k_abx: float) -> float:
     covariance 4M³; power iteration k_pi·(8M²+12M); v_1 = Γ^H u_1 8M²+4M; two
     autocorrelation polynomials 8M(M−1); symmetric Aberth sweeps k·(n/2)·(25n+21) with
     n = 2M−2 (per tracked root: Horner for P and P′ 16n, n−1 reciprocal terms at 9 flops,
-    mirror + update 30); selection 2·20(n/2); Eq.(15) 8M²+8M+20."""
+    mirror + update 30); selection 2·20(n/2); 2 Newton polish steps per axis 2·2·(16n+30);
+    Eq.(15) 8M²+8M+20."""
     n = 2 * M - 2
+    polish = 2 * 2 * (16.0 * n + 30.0)       # 2 Newton steps on the selected root, 2 axes
     return (4.0 * M ** 3 + k_pi * (8.0 * M * M + 12.0 * M) + 8.0 * M * M + 4.0 * M
             + 8.0 * M * (M - 1) + (k_aby + k_abx) * (n / 2.0) * (25.0 * n + 21.0) + 20.0 * n
-            + 8.0 * M * M + 8.0 * M + 20.0)
+            + polish + 8.0 * M * M + 8.0 * M + 20.0)
 
 
 class ClockSampler:
