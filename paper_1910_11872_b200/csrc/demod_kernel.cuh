@@ -38,7 +38,7 @@ constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.032), then polish
 constexpr int kPolishSteps = 2;       // Newton steps on the selected root after the sweeps
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
-constexpr float kCosTauOmega = 0.99995000042f;  // cos(1e-2): "distinct frequency" test
+constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
 constexpr float kLowAmp = 1e-4f;      // LOW_AMPLITUDE threshold
 
@@ -211,35 +211,30 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
     return it;
 }
 
-// Root closest to the unit circle (min |ln|z||, via the monotone tanh(|ln r|) =
-// |r²−1|/(r²+1); a root and its mirror tie) and the margin to the best root of a
-// different frequency.
+// Root closest to the unit circle: argmin |ln|z|| = ½|ln|z|²| (one MUFU.LG2 per root, no
+// division; a root and its mirror tie, P:L208 [R6]) and the margin, in |ln|z|| units, to the
+// best root of a different frequency (|arg z − arg z_b| > τ_ω) for the AMBIGUOUS flag.
 template <int K>
 __device__ __forceinline__ float2 select_root(const cx2 (&zp)[K], float& margin) {
-    float2 z[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) z[i] = cx2_f2(zp[i]);
-    float best = CUDART_INF_F;
+    float best = CUDART_INF_F, rb2 = 1.0f;
     float2 zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
+    float d[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        const float r2 = cabs2(z[i]);
-        const float d = fabsf(r2 - 1.0f) / (r2 + 1.0f);
-        if (d < best) { best = d; zb = z[i]; }
+        const float2 z = cx2_f2(zp[i]);
+        const float r2 = cabs2(z);
+        d[i] = fabsf(__log2f(r2));
+        if (d[i] < best) { best = d[i]; zb = z; rb2 = r2; }
     }
-    const float rb = sqrtf(cabs2(zb));
     float second = CUDART_INF_F;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-        const float r2 = cabs2(z[i]);
-        const float d = fabsf(r2 - 1.0f) / (r2 + 1.0f);
-        const float dot = fmaf(z[i].x, zb.x, z[i].y * zb.y);        // Re(z_i conj(z_b))
-        if (dot < kCosTauOmega * sqrtf(r2) * rb) second = fminf(second, d);
+        const float2 z = cx2_f2(zp[i]);
+        const float dot = fmaf(z.x, zb.x, z.y * zb.y);        // Re(z_i conj(z_b)) = |z_i||z_b| cos Δ
+        const bool distinct = dot < 0.0f || dot * dot < kCos2TauOmega * cabs2(z) * rb2;
+        if (distinct) second = fminf(second, d[i]);
     }
-    // |ln r| = atanh(d)
-    const float a1 = 0.5f * __logf((1.0f + best) / (1.0f - best));
-    const float a2 = second < 1.0f ? 0.5f * __logf((1.0f + second) / (1.0f - second)) : CUDART_INF_F;
-    margin = a2 - a1;
+    margin = (second - best) * 0.34657359f;                  // log2 → |ln r|: × ln2/2
     return zb;
 }
 
@@ -249,18 +244,25 @@ __device__ __forceinline__ float2 select_root(const cx2 (&zp)[K], float& margin)
 template <int M>
 __device__ __forceinline__ float2 music_coeffs(const float2 (&q)[M], cx2 (&c)[2 * M - 1]) {
     float n2 = 0.0f;
+    cx2 qp[M], qnj[M];   // q_i and −j·q_i; q_i·conj(b) = re(b)·q_i + im(b)·(−j·q_i)
 #pragma unroll
-    for (int i = 0; i < M; ++i) n2 += cabs2(q[i]);
+    for (int i = 0; i < M; ++i) {
+        n2 += cabs2(q[i]);
+        qp[i] = cx2_make(q[i].x, q[i].y);
+        qnj[i] = cx2_make(q[i].y, -q[i].x);
+    }
     c[M - 1] = cx2_make(float(M) - n2, 0.0f);
     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int d = 1; d < M; ++d) {
-        float2 r = make_float2(0.0f, 0.0f);
+        cx2 r = 0ull;
 #pragma unroll
-        for (int i = 0; i + d < M; ++i) r = cfmac(q[i], q[i + d], r);
-        c[M - 1 + d] = cx2_make(-r.x, -r.y);
-        c[M - 1 - d] = cx2_make(-r.x, r.y);
-        if (d == 1) r1 = r;
+        for (int i = 0; i + d < M; ++i)
+            r = fma2(cx2_bcast(q[i + d].x), qp[i], fma2(cx2_bcast(q[i + d].y), qnj[i], r));
+        const float2 rf = cx2_f2(r);
+        c[M - 1 + d] = cx2_make(-rf.x, -rf.y);
+        c[M - 1 - d] = cx2_make(-rf.x, rf.y);
+        if (d == 1) r1 = rf;
     }
     const float n = cabs2(r1);
     if (!(n > 0.0f)) return make_float2(1.0f, 0.0f);
@@ -282,28 +284,33 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
     constexpr int N = 2 * M - 2;                 // polynomial degree
     constexpr int O0 = (M - 1) / 2;              // o_i = i − O0  [R2]
     constexpr int TW = kBX + M - 1;
-    constexpr int TH = kBY + M - 1;
     constexpr int NOFF = M * (M - 1) / 2;
-    __shared__ float2 tile[TH * TW];
+    // One private halo tile per warp (row py, M rows × (32+M−1) columns): warps then move
+    // through frames independently (__syncwarp only), so a warp with slow pixels never holds
+    // the other three at a CTA barrier.  Re-staging the M−1 overlap rows per warp costs ~10
+    // LDG/STS per pixel of a ~7k-instruction pixel.
+    __shared__ float2 tiles[kBY][M * TW];
+    float2* tile = tiles[threadIdx.y];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
     const int px = x0 + tx, py = y0 + ty;
     const size_t plane = (size_t)H * (size_t)W;
+    if (py >= H) return;                         // warp-uniform: the whole row is outside
 
     for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
         const float2* __restrict__ frame = frames + (size_t)f * plane;
-        // ---- a1: stage the clamped halo tile (Eq.(2) window support, [R1] clamp) ----
-        for (int idx = ty * kBX + tx; idx < TH * TW; idx += kThreads) {
+        // ---- a1: stage the clamped halo rows (Eq.(2) window support, [R1] clamp) ----
+        for (int idx = tx; idx < M * TW; idx += kBX) {
             const int r = idx / TW, cc = idx - r * TW;
-            const int gy = min(max(y0 - O0 + r, 0), H - 1);
+            const int gy = min(max(py - O0 + r, 0), H - 1);
             const int gx = min(max(x0 - O0 + cc, 0), W - 1);
             tile[idx] = __ldg(frame + (size_t)gy * W + gx);
         }
-        __syncthreads();
+        __syncwarp();
 
-        if (px < W && py < H) {
-            const float2* win = tile + ty * TW + tx;   // Γ_w(i,k) = win[i*TW + k]
+        if (px < W) {
+            const float2* win = tile + tx;             // Γ_w(i,k) = win[i*TW + k]
             uint8_t fl = 0;
             if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
                 fl |= kFlagBorder;
@@ -506,7 +513,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 atomicAdd(counters + 3, (unsigned long long)n_abx);
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
