@@ -63,7 +63,7 @@ enum {
 /* Window sizes with an instantiated kernel (window_len = M = 2L+1 in the paper, P:L98,
  * P:L130; even M allowed [R2]). */
 #define BOS_WINDOW_LEN_MIN 3
-#define BOS_WINDOW_LEN_MAX 16
+#define BOS_WINDOW_LEN_MAX 32
 #define BOS_MODEL_ORDER 3   /* Eq.(3): φ_w = α + ω_x x + ω_y y, three parameters [R3] */
 
 /*

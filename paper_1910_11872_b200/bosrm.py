@@ -28,7 +28,7 @@ FLAG_NONFINITE = 1 << 4
 FLAG_BORDER = 1 << 5
 
 WINDOW_LEN_MIN = 3
-WINDOW_LEN_MAX = 16
+WINDOW_LEN_MAX = 32
 MODEL_ORDER = 3
 
 # name -> (restype, argtypes); must match include/bos_rootmusic.h

@@ -22,7 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "bosrm")
 LIB = os.path.join(PKG, "libbosrm.so")
 
-WINDOW_LENS = list(range(3, 17))      # BOS_WINDOW_LEN_MIN .. BOS_WINDOW_LEN_MAX
+WINDOW_LENS = list(range(3, 33))      # BOS_WINDOW_LEN_MIN .. BOS_WINDOW_LEN_MAX
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC,
                   "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -32,6 +32,22 @@ LaunchFn pick(int M) {
         case 14: return bos::launch_demod<14, COUNT>;
         case 15: return bos::launch_demod<15, COUNT>;
         case 16: return bos::launch_demod<16, COUNT>;
+        case 17: return bos::launch_demod<17, COUNT>;
+        case 18: return bos::launch_demod<18, COUNT>;
+        case 19: return bos::launch_demod<19, COUNT>;
+        case 20: return bos::launch_demod<20, COUNT>;
+        case 21: return bos::launch_demod<21, COUNT>;
+        case 22: return bos::launch_demod<22, COUNT>;
+        case 23: return bos::launch_demod<23, COUNT>;
+        case 24: return bos::launch_demod<24, COUNT>;
+        case 25: return bos::launch_demod<25, COUNT>;
+        case 26: return bos::launch_demod<26, COUNT>;
+        case 27: return bos::launch_demod<27, COUNT>;
+        case 28: return bos::launch_demod<28, COUNT>;
+        case 29: return bos::launch_demod<29, COUNT>;
+        case 30: return bos::launch_demod<30, COUNT>;
+        case 31: return bos::launch_demod<31, COUNT>;
+        case 32: return bos::launch_demod<32, COUNT>;
         default: return nullptr;
     }
 }

@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "demod_kernel.cuh"
+#include "demod_wide.cuh"
 #include "launch.h"
 
 #ifndef BOS_INST_M
@@ -17,7 +18,11 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
     const dim3 block(kBX, kBY, 1);
     const dim3 grid((unsigned)((W + kBX - 1) / kBX), (unsigned)((H + kBY - 1) / kBY),
                     (unsigned)std::min(n_frames, 65535));
-    demod_kernel<M, COUNT><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, counters);
+    if constexpr (M >= kWideMinM) {
+        demod_wide_kernel<M, COUNT><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, counters);
+    } else {
+        demod_kernel<M, COUNT><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, counters);
+    }
     return cudaGetLastError();
 }
 

@@ -1,0 +1,363 @@
+// demod_wide.cuh — warp-per-pixel root-MUSIC demodulation for large windows (M = 17…32).
+//
+// Same algorithm and arithmetic as demod_kernel.cuh (a1–a7, symmetric Aberth, Newton polish),
+// laid out for M where a thread can no longer hold R_y (M(M+1)/2 complex) in registers:
+//
+// * one CTA = 4 warps = 4 image rows × a 32-pixel row segment; the CTA stages the clamped
+//   (4+M−1)×(32+M−1) halo once per frame (odd row stride → conflict-free column reads);
+// * each warp walks its 32 pixels left to right; lane i owns row i of R_y.  R_y is formed in
+//   full at the first pixel of the segment and then slid one column per pixel with a rank-2
+//   update  R += a_new a_new^H − a_old a_old^H  (2M instead of M² complex MACs per lane; the
+//   refresh every 32 pixels bounds FP32 drift to ~32 ε‖R‖ — cf. parity tests);
+// * power iteration, v_1 = Γ^H u_1 and the autocorrelation coefficients use lane-distributed
+//   vectors and warp shuffles; the polynomial coefficients go to a per-warp SMEM buffer that
+//   every lane reads by broadcast during Horner;
+// * Aberth: lane k owns tracked root z_k (K = M−1 ≤ 31 roots), simultaneous (Jacobi) update,
+//   the other roots and mirrors arrive by shuffle; warp-reduced stop test, argmin selection
+//   and margin; two Newton polish steps on the selected root;
+// * Eq.(15) row sums per lane, warp reduction, lane 0 stores phase + flags.
+#pragma once
+
+#include "demod_kernel.cuh"
+
+namespace bos {
+
+constexpr int kWideMinM = 17;
+
+__device__ __forceinline__ cx2 shfl_cx2(cx2 v, int src) {
+    return (cx2)__shfl_sync(0xffffffffu, (unsigned long long)v, src);
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float2 warp_sum2(float2 v) { return make_float2(warp_sum(v.x), warp_sum(v.y)); }
+
+// Horner on coefficients in shared memory (broadcast reads): Newton ratio P/P′ with the
+// reversed-polynomial evaluation for |z| > 1 (see newton_ratio).
+template <int N>
+__device__ __forceinline__ float2 newton_ratio_smem(const cx2* __restrict__ c, float2 zi) {
+    const float m2 = cabs2(zi);
+    const bool outside = m2 > 1.0f;
+    const float2 v = outside ? cscale(zi, __fdividef(1.0f, m2)) : zi;
+    const cx2 V = cx2_make(v.x, v.y);
+    const cx2 Vj = mul2(cx2_make(v.y, v.x), cx2_make(-1.0f, 1.0f));
+    cx2 p = c[N];
+    cx2 dp = 0ull;
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+        dp = cmad2(dp, V, Vj, p);
+        p = cmad2(p, V, Vj, c[k]);
+    }
+    float2 num = cx2_f2(p), den = cx2_f2(dp);
+    if (outside) {
+        const float2 q = cconj(num), dq = cconj(den), u = cconj(v);
+        num = cmul(zi, q);
+        den = csub(cscale(q, float(N)), cmul(u, dq));
+    }
+    return cdiv(num, den);
+}
+
+template <int N>
+__device__ __forceinline__ float2 newton_on_derivative_smem(const cx2* __restrict__ c, float2 z) {
+    const cx2 V = cx2_make(z.x, z.y);
+    const cx2 Vj = mul2(cx2_make(z.y, z.x), cx2_make(-1.0f, 1.0f));
+    cx2 p = c[N];
+    cx2 dp = 0ull, ddp = 0ull;
+#pragma unroll
+    for (int k = N - 1; k >= 0; --k) {
+        ddp = cmad2(ddp, V, Vj, dp);
+        dp = cmad2(dp, V, Vj, p);
+        p = cmad2(p, V, Vj, c[k]);
+    }
+    return cdiv(cx2_f2(dp), cscale(cx2_f2(ddp), 2.0f));
+}
+
+template <int M>
+constexpr int wide_min_blocks() { return M <= 24 ? 3 : 2; }
+
+template <int M, bool COUNT>
+__global__ void __launch_bounds__(kThreads, wide_min_blocks<M>())
+demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
+                  const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
+                  unsigned long long* __restrict__ counters) {
+    static_assert(M >= kWideMinM && M <= 32, "wide kernel: 17 <= M <= 32");
+    constexpr int N = 2 * M - 2;                 // polynomial degree
+    constexpr int K = N / 2;                     // tracked (inside) roots, one per lane
+    constexpr int O0 = (M - 1) / 2;              // o_i = i − O0  [R2]
+    constexpr int TW = (kBX + M - 1) | 1;        // odd float2 stride: conflict-free row-per-lane reads
+    constexpr int TH = kBY + M - 1;
+    __shared__ float2 tile[TH * TW];
+    __shared__ cx2 coef_s[kBY][N + 1];
+
+    const int lane = threadIdx.x, warp = threadIdx.y;
+    const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
+    const int py = y0 + warp;
+    const size_t plane = (size_t)H * (size_t)W;
+    const int ri = lane < M ? lane : M - 1;      // lane's row / column of the window (clamped)
+    const bool rl = lane < M;
+    const bool kl = lane < K;
+    cx2* coef = coef_s[warp];
+    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+
+    for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
+        const float2* __restrict__ frame = frames + (size_t)f * plane;
+        // ---- a1: stage the clamped halo tile ----
+        for (int idx = warp * kBX + lane; idx < TH * (kBX + M - 1); idx += kThreads) {
+            const int r = idx / (kBX + M - 1), cc = idx - r * (kBX + M - 1);
+            const int gy = min(max(y0 - O0 + r, 0), H - 1);
+            const int gx = min(max(x0 - O0 + cc, 0), W - 1);
+            tile[r * TW + cc] = __ldg(frame + (size_t)gy * W + gx);
+        }
+        __syncthreads();
+
+        if (py < H) {
+            const float2* wrow = tile + warp * TW;   // window of pixel p: Γ(i,k) = wrow[i*TW + p + k]
+            cx2 R[M];                                // lane i: row i of R_y
+            bool rebuild = true;                     // full R at the segment start / after non-finite data
+#pragma unroll 1
+            for (int p = 0; p < kBX; ++p) {
+                const int px = x0 + p;
+                if (px >= W) break;                  // warp-uniform
+                // ---- a2: R_y row `ri` (full at the segment start, then rank-2 slides) ----
+                if (rebuild) {
+#pragma unroll
+                    for (int j = 0; j < M; ++j) R[j] = 0ull;
+#pragma unroll 1
+                    for (int k = p; k < p + M; ++k) {
+                        const float2 g = wrow[ri * TW + k];
+                        const cx2 A = cx2_make(g.x, g.y), Anj = cx2_make(g.y, -g.x);
+#pragma unroll
+                        for (int j = 0; j < M; ++j) {
+                            const float2 b = wrow[j * TW + k];
+                            R[j] = fma2(cx2_bcast(b.x), A, fma2(cx2_bcast(b.y), Anj, R[j]));
+                        }
+                    }
+                } else {
+                    const float2 go = wrow[ri * TW + p - 1], gn = wrow[ri * TW + p + M - 1];
+                    const cx2 Ao = cx2_make(go.x, go.y), Aonj = cx2_make(go.y, -go.x);
+                    const cx2 An = cx2_make(gn.x, gn.y), Annj = cx2_make(gn.y, -gn.x);
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        const float2 bo = wrow[j * TW + p - 1], bn = wrow[j * TW + p + M - 1];
+                        R[j] = fma2(cx2_bcast(bn.x), An, fma2(cx2_bcast(bn.y), Annj, R[j]));
+                        R[j] = fma2(cx2_bcast(-bo.x), Ao, fma2(cx2_bcast(-bo.y), Aonj, R[j]));
+                    }
+                }
+                // diagonal element R_ii and sub-diagonal R_{i,i−1} of this lane's row
+                float dii = 0.0f;
+                float2 sub = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    if (j == lane) dii = cx2_re(R[j]);
+                    if (j + 1 == lane) sub = cx2_f2(R[j]);
+                }
+                const float trace = warp_sum(rl ? dii : 0.0f);
+
+                uint8_t fl = 0;
+                if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
+                    fl |= kFlagBorder;
+                float result;
+                int n_pow = 0, n_aby = 0, n_abx = 0;
+                rebuild = !isfinite(trace);          // NaN/Inf never leave R by subtraction
+                if (!isfinite(trace)) {
+                    fl |= kFlagNonfinite;
+                    result = CUDART_NAN_F;
+                } else {
+                    // ---- a3: power iteration, lane i holds u_i ----
+                    const float2 r1 = warp_sum2(rl ? sub : make_float2(0.0f, 0.0f));   // Σ_i R[i+1][i]
+                    float2 e = make_float2(1.0f, 0.0f);
+                    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+                    cx2 u;
+                    {
+                        float2 t = make_float2(rsqrtf(float(M)), 0.0f), ul = t;
+#pragma unroll
+                        for (int j = 0; j < M; ++j) {
+                            if (j == lane) ul = t;
+                            t = cmul(t, e);
+                        }
+                        u = rl ? cx2_make(ul.x, ul.y) : 0ull;
+                    }
+                    bool pow_ok = false;
+                    for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                        cx2 y = 0ull;
+#pragma unroll
+                        for (int j = 0; j < M; ++j) {
+                            const cx2 uj = shfl_cx2(u, j);
+                            const cx2 ujj = mul2(cx2_make(cx2_im(uj), cx2_re(uj)), cx2_make(-1.0f, 1.0f));
+                            y = fma2(cx2_bcast(cx2_re(R[j])), uj, fma2(cx2_bcast(cx2_im(R[j])), ujj, y));
+                        }
+                        if (!rl) y = 0ull;
+                        const float nrm2 = warp_sum(cabs2(cx2_f2(y)));
+                        const cx2 yn = mul2(y, cx2_bcast(rsqrtf(nrm2)));
+                        const float diff = warp_sum(cabs2(cx2_f2(sub2(yn, u))));
+                        u = yn;
+                        ++n_pow;
+                        if (diff < kPowerTol) { pow_ok = true; break; }
+                    }
+                    // v_1 ∝ Γ_w^H u_1, lane k holds v_k
+                    cx2 v = 0ull;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        const float2 g = wrow[i * TW + p + ri];
+                        const cx2 ui = shfl_cx2(u, i);
+                        const cx2 uinj = mul2(cx2_make(cx2_im(ui), cx2_re(ui)), kPosNeg);
+                        v = fma2(cx2_bcast(g.x), ui, fma2(cx2_bcast(g.y), uinj, v));
+                    }
+                    if (!rl) v = 0ull;
+                    v = mul2(v, cx2_bcast(rsqrtf(warp_sum(cabs2(cx2_f2(v))))));
+
+                    // ---- a4 + a5 per axis ----
+                    float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
+                    float my = CUDART_INF_F, mx = CUDART_INF_F;
+                    bool aby_ok = false, abx_ok = false;
+#pragma unroll 1
+                    for (int axis = 0; axis < 2; ++axis) {
+                        const cx2 q = axis ? v : u;
+                        const cx2 qnj = mul2(cx2_make(cx2_im(q), cx2_re(q)), kPosNeg);   // −j·q
+                        // lane d: r_d = Σ_i q_i conj(q_{i+d}) = Σ_i re(q_{i+d})·q_i + im(q_{i+d})·(−j q_i)
+                        const int d = lane;
+                        cx2 r = 0ull;
+#pragma unroll
+                        for (int i = 0; i < M - 1; ++i) {
+                            const cx2 qi = shfl_cx2(q, i), qinj = shfl_cx2(qnj, i);
+                            const cx2 qid = shfl_cx2(q, min(i + d, 31));
+                            const bool valid = d >= 1 && i + d < M;
+                            const cx2 t = fma2(cx2_bcast(cx2_re(qid)), qi, fma2(cx2_bcast(cx2_im(qid)), qinj, r));
+                            r = valid ? t : r;
+                        }
+                        const float n2 = warp_sum(cabs2(cx2_f2(q)));
+                        const float2 rf = cx2_f2(r);
+                        if (lane == 0) coef[M - 1] = cx2_make(float(M) - n2, 0.0f);
+                        if (d >= 1 && d < M) {
+                            coef[M - 1 + d] = cx2_make(-rf.x, -rf.y);
+                            coef[M - 1 - d] = cx2_make(-rf.x, rf.y);
+                        }
+                        const float2 r1q = cx2_f2(shfl_cx2(r, 1));
+                        float2 rot = make_float2(1.0f, 0.0f);
+                        if (cabs2(r1q) > 0.0f) rot = cscale(cconj(r1q), rsqrtf(cabs2(r1q)));
+                        __syncwarp();
+                        // Aberth–Ehrlich, lane k owns root k (simultaneous update)
+                        float2 z = kl ? cmul(kTemplateRoots[bos_template_offset(M) + lane], rot) : make_float2(0.0f, 0.0f);
+                        cx2 zp = f2_cx2(z), zmp = kl ? mirror(zp) : 0ull;
+                        int it = 0;
+                        bool ok = false;
+                        for (; it < kAberthMaxIt; ++it) {
+                            const float2 ratio = newton_ratio_smem<N>(coef, z);
+                            const bool near = fabsf(1.0f - cabs2(z)) < kNearCircle;
+                            const cx2 ziC = mul2(zp, kPosNeg);
+                            const cx2 kNegPos = cx2_make(-1.0f, 1.0f);
+                            cx2 s = 0ull;
+#pragma unroll
+                            for (int j = 0; j < K; ++j) {
+                                const cx2 zj = shfl_cx2(zp, j), zmj = shfl_cx2(zmp, j);
+                                const cx2 d1 = fma2(zj, kNegPos, ziC);
+                                const float q1 = fmaf(cx2_re(d1), cx2_re(d1), cx2_im(d1) * cx2_im(d1));
+                                const cx2 t1 = fma2(cx2_bcast(rcp_approx(q1)), d1, s);
+                                s = (j != lane) ? t1 : s;
+                                const cx2 d2 = fma2(zmj, kNegPos, ziC);
+                                const float q2 = fmaf(cx2_re(d2), cx2_re(d2), cx2_im(d2) * cx2_im(d2));
+                                const cx2 t2 = fma2(cx2_bcast(rcp_approx(q2)), d2, s);
+                                s = (j != lane || !near) ? t2 : s;
+                            }
+                            const float2 sf = cx2_f2(s);
+                            const float2 dd = make_float2(1.0f - (ratio.x * sf.x - ratio.y * sf.y),
+                                                          -(ratio.x * sf.y + ratio.y * sf.x));
+                            float2 w = cdiv(ratio, dd);
+                            if (near) w = newton_on_derivative_smem<N>(coef, z);
+                            float w2 = cabs2(w);
+                            if (!(w2 < 1e30f) || !kl) {
+                                w = make_float2(0.0f, 0.0f);
+                                w2 = 0.0f;
+                            }
+                            z = csub(z, w);
+                            zp = f2_cx2(z);
+                            zmp = kl ? mirror(zp) : 0ull;
+                            if (warp_max(w2) < kAberthTol2) { ok = true; ++it; break; }
+                        }
+                        // selection: argmin |log2 |z|²| over lanes, margin to a different frequency
+                        const float r2 = cabs2(z);
+                        const float dl = kl ? fabsf(__log2f(r2)) : CUDART_INF_F;
+                        const float best = warp_min(dl);
+                        const int bl = __ffs(__ballot_sync(0xffffffffu, dl == best)) - 1;
+                        float2 zb = cx2_f2(shfl_cx2(zp, bl < 0 ? 0 : bl));
+                        if (!(best < CUDART_INF_F)) zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
+                        const float rb2 = cabs2(zb);
+                        const float dot = fmaf(z.x, zb.x, z.y * zb.y);
+                        const bool distinct = kl && (dot < 0.0f || dot * dot < kCos2TauOmega * r2 * rb2);
+                        const float second = warp_min(distinct ? dl : CUDART_INF_F);
+                        const float marg = (second - best) * 0.34657359f;
+#pragma unroll 1
+                        for (int t = 0; t < kPolishSteps; ++t) {
+                            const float2 wp = newton_ratio_smem<N>(coef, zb);
+                            if (cabs2(wp) < 1e30f) zb = csub(zb, wp);
+                        }
+                        __syncwarp();                // coefficient buffer reused by the next axis
+                        if (axis == 0) { zy = zb; my = marg; aby_ok = ok; n_aby = it; }
+                        else { zx = zb; mx = marg; abx_ok = ok; n_abx = it; }
+                    }
+                    if (!pow_ok || !aby_ok || !abx_ok || !isfinite(zy.x + zy.y + zx.x + zx.y))
+                        fl |= kFlagNonconverged;
+                    if (fminf(my, mx) < kTauSel) fl |= kFlagAmbiguous;
+
+                    // ---- a6: Eq.(15); lane i forms row_i = Σ_k Γ(i,k) ẑ_x^{o_k} ----
+                    const float2 hx = cscale(zx, rsqrtf(cabs2(zx)));
+                    const float2 hy = cscale(zy, rsqrtf(cabs2(zy)));
+                    float2 tw = make_float2(1.0f, 0.0f);
+#pragma unroll
+                    for (int k = 0; k < O0; ++k) tw = cmul(tw, cconj(hx));
+                    cx2 row = 0ull;
+#pragma unroll
+                    for (int k = 0; k < M; ++k) {
+                        const float2 g = wrow[ri * TW + p + k];
+                        const cx2 T = cx2_make(tw.x, tw.y), Tj = cx2_make(-tw.y, tw.x);
+                        row = fma2(cx2_bcast(g.x), T, fma2(cx2_bcast(g.y), Tj, row));
+                        tw = cmul(tw, hx);
+                    }
+                    // q_i = conj(ẑ_y)^{o_i} for this lane's row
+                    float2 qy = make_float2(1.0f, 0.0f), qi = qy;
+#pragma unroll
+                    for (int i = 0; i < O0; ++i) qy = cmul(qy, hy);
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        if (i == lane) qi = qy;
+                        qy = cmul(qy, cconj(hy));
+                    }
+                    float2 cs = rl ? cmul(cx2_f2(row), qi) : make_float2(0.0f, 0.0f);
+                    cs = warp_sum2(cs);
+                    if (!(cabs2(cs) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
+                    float a = atan2f(cs.y, cs.x);
+                    if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
+                    if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
+                    if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
+                    result = a;
+                }
+                if (lane == 0) {
+                    const size_t o = (size_t)f * plane + (size_t)py * W + px;
+                    out[o] = result;
+                    if (flags != nullptr) flags[o] = fl;
+                    if (COUNT) {
+                        atomicAdd(counters + 0, 1ull);
+                        atomicAdd(counters + 1, (unsigned long long)n_pow);
+                        atomicAdd(counters + 2, (unsigned long long)n_aby);
+                        atomicAdd(counters + 3, (unsigned long long)n_abx);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace bos

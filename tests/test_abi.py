@@ -69,7 +69,7 @@ def test_error_codes_without_device(L):
     assert f(None, 1, 64, 64, 8, 2, None, None, None, None) == bosrm.BOS_ERR_UNSUPPORTED
     # window_len out of range
     assert f(None, 1, 64, 64, 2, 3, None, None, None, None) == bosrm.BOS_ERR_INVALID_ARG
-    assert f(None, 1, 64, 64, 17, 3, None, None, None, None) == bosrm.BOS_ERR_UNSUPPORTED
+    assert f(None, 1, 64, 64, 33, 3, None, None, None, None) == bosrm.BOS_ERR_UNSUPPORTED
     # frame smaller than the window, no frames, NULL pointers
     assert f(None, 1, 7, 64, 8, 3, None, None, None, None) == bosrm.BOS_ERR_INVALID_ARG
     assert f(None, 0, 64, 64, 8, 3, None, None, None, None) == bosrm.BOS_ERR_INVALID_ARG

@@ -88,11 +88,13 @@ def test_c2_pair_parity(M, snr, full):
 
 
 # ------------------------------------------------------------------- ragged / all M
-@pytest.mark.parametrize("M", list(range(3, 17)))
+@pytest.mark.parametrize("M", list(range(3, 33)))
 def test_all_window_lengths_ragged_frame(M):
-    """Every instantiated M on a ragged 37×45 frame (not a multiple of the 32×4 tile)."""
+    """Every instantiated M on a ragged frame (not a multiple of the 32×4 tile; for the
+    warp-per-pixel kernel (M ≥ 17) wider than one 32-pixel segment, so the sliding R_y
+    update runs)."""
     w = synth.workload("C2", H=37, W=45, seed=M)
-    H, W = 37, 45
+    H, W = (37, 45) if M < 17 else (M + 6, 75)
     # smooth carrier fringe with mild phase, 10 dB
     f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M), 5, snr_db=10.0)
     g, gfl = run_gpu(f, M)
@@ -103,7 +105,7 @@ def test_all_window_lengths_ragged_frame(M):
 
 
 def test_minimum_frame_equals_window():
-    for M in (3, 8, 16):
+    for M in (3, 8, 16, 17, 32):
         f = synth.make_frame(synth.workload("C3", H=M, W=M, seed=2), 3, snr_db=20.0)
         g, _ = run_gpu(f, M)
         o, ofl = R.demod_frame(f.numpy(), M)
@@ -173,7 +175,7 @@ def test_error_codes_on_device():
         bosrm.BOS_ERR_INVALID_ARG
     assert L.bos_rootmusic_demod(f.data_ptr(), 1, 32, 32, 8, 3, None, f.data_ptr(), None, s) == \
         bosrm.BOS_ERR_INVALID_ARG
-    assert L.bos_rootmusic_demod(f.data_ptr(), 1, 32, 32, 17, 3, None, out.data_ptr(), None, s) == \
+    assert L.bos_rootmusic_demod(f.data_ptr(), 1, 40, 40, 33, 3, None, out.data_ptr(), None, s) == \
         bosrm.BOS_ERR_UNSUPPORTED
     with pytest.raises(bosrm.BosError):
         bosrm.bos_rootmusic_demod(f, 2)
@@ -209,7 +211,7 @@ def test_c3_full_size_sampled_parity():
         assert_parity(g[j][pix], o[j], ofl[j], f"C3 frame {frames[j + 1]}")
 
 
-@pytest.mark.parametrize("M", [4, 5, 8, 11, 16])
+@pytest.mark.parametrize("M", [4, 5, 8, 11, 16, 17, 24, 32])
 @pytest.mark.parametrize("snr", [None, 40.0, 25.0])
 def test_high_snr_and_noise_free_parity(M, snr):
     """Near-double roots on the unit circle (noise-free / high SNR) on a 64×72 crop-sized
@@ -219,3 +221,17 @@ def test_high_snr_and_noise_free_parity(M, snr):
     g, _ = run_gpu(f, M)
     o, ofl = R.demod_frame(f.numpy(), M)
     assert_parity(g, o, ofl, f"high-SNR M={M} snr={snr}", max_excluded_frac=0.02)
+
+
+@pytest.mark.parametrize("M", [17, 25])
+def test_wide_kernel_nonfinite_does_not_leak_along_the_segment(M):
+    """A NaN sample poisons only the windows that contain it: the sliding R_y update of the
+    warp-per-pixel kernel rebuilds R after a non-finite window."""
+    H, W = M + 8, 70
+    f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=5), 4, snr_db=15.0).clone()
+    f[H // 2, 10] = complex(float("nan"), 0.0)
+    g, gfl = run_gpu(f, M)
+    o, ofl = R.demod_frame(f.numpy(), M)
+    bad = (ofl & R.FLAG_NONFINITE) != 0
+    assert np.all(np.isnan(g[bad])) and np.all(gfl[bad] & bosrm.FLAG_NONFINITE)
+    assert_parity(g, o, ofl, f"wide NaN M={M}", max_excluded_frac=0.9)
