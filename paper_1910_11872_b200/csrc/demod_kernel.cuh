@@ -36,7 +36,9 @@ constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyon
 constexpr float kPowerTol = 1e-10f;   // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2))
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.032), then polish
-constexpr int kPolishSteps = 2;       // Newton steps on the selected root after the sweeps
+constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
+constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
+constexpr float kPolishTol2 = 1e-12f;
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
@@ -448,13 +450,15 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     const int its = aberth_sym<N>(c, z, ok);
                     float marg;
                     float2 zs = select_root<N / 2>(z, marg);
-                    // The sweeps stop once every root moved < kAberthStop (cubic convergence
-                    // leaves ~1e-5 there); two Newton steps on the selected root alone then
-                    // make it FP32-accurate (quadratic) at 1/7 of a sweep each.
+                    // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
+                    // ~1e-5 there); Newton steps on the selected root alone then make it
+                    // FP32-accurate (quadratic) at 1/(M−1) of a sweep each.
 #pragma unroll 1
-                    for (int t = 0; t < kPolishSteps; ++t) {
+                    for (int t = 0; t < kPolishMax; ++t) {
                         const float2 w = newton_ratio<N>(c, zs);
-                        if (cabs2(w) < 1e30f) zs = csub(zs, w);
+                        const float w2 = cabs2(w);
+                        if (w2 < 1e30f) zs = csub(zs, w);
+                        if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
                     }
                     if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
                     else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }

@@ -299,9 +299,11 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float second = warp_min(distinct ? dl : CUDART_INF_F);
                         const float marg = (second - best) * 0.34657359f;
 #pragma unroll 1
-                        for (int t = 0; t < kPolishSteps; ++t) {
+                        for (int t = 0; t < kPolishMax; ++t) {   // warp-uniform: zb is the same on all lanes
                             const float2 wp = newton_ratio_smem<N>(coef, zb);
-                            if (cabs2(wp) < 1e30f) zb = csub(zb, wp);
+                            const float w2 = cabs2(wp);
+                            if (w2 < 1e30f) zb = csub(zb, wp);
+                            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
                         }
                         __syncwarp();                // coefficient buffer reused by the next axis
                         if (axis == 0) { zy = zb; my = marg; aby_ok = ok; n_aby = it; }
