@@ -84,6 +84,41 @@ __device__ __forceinline__ float2 newton_on_derivative_smem(const cx2* __restric
     return cdiv(cx2_f2(dp), cscale(cx2_f2(ddp), 2.0f));
 }
 
+// P(z)/P′(z) at ONE point z with the whole warp: lane l sums the terms k = 2l, 2l+1 (the
+// coefficient buffer is zero-padded to 64), v^{2l−1} by binary exponentiation, then a warp
+// reduction — ~5 dependent complex products + 5 shuffle levels instead of an N-step Horner
+// chain on every lane.  Reversed evaluation for |z| > 1 as in newton_ratio.
+template <int N>
+__device__ __forceinline__ float2 newton_ratio_warp(const cx2* __restrict__ c, float2 zi, int lane) {
+    const float m2 = cabs2(zi);
+    const bool outside = m2 > 1.0f;
+    const float2 v = outside ? cscale(zi, __fdividef(1.0f, m2)) : zi;
+    const float2 v2 = cmul(v, v);
+    // q = (v²)^{l−1} for l ≥ 1 (5-bit exponent)
+    const int e = lane > 0 ? lane - 1 : 0;
+    float2 q = make_float2(1.0f, 0.0f), b = v2;
+#pragma unroll
+    for (int bit = 0; bit < 5; ++bit) {
+        if ((e >> bit) & 1) q = cmul(q, b);
+        b = cmul(b, b);
+    }
+    const float2 pm1 = cmul(q, v);                                  // v^{2l−1}
+    const float2 pw = lane > 0 ? cmul(pm1, v) : make_float2(1.0f, 0.0f);   // v^{2l}
+    const float2 c0 = cx2_f2(c[2 * lane]), c1 = cx2_f2(c[2 * lane + 1]);
+    const float2 pp = cmul(pw, cfma(c1, v, c0));                    // c0 v^{2l} + c1 v^{2l+1}
+    const float a = float(2 * lane);
+    const float2 dterm = cfma(cscale(c1, a + 1.0f), v, cscale(c0, a));   // 2l·c0 + (2l+1)·c1·v
+    const float2 dd = lane > 0 ? cmul(pm1, dterm) : c1;              // d/dv of the two terms
+    const float2 P = warp_sum2(pp), D = warp_sum2(dd);
+    float2 num = P, den = D;
+    if (outside) {
+        const float2 qq = cconj(num), dq = cconj(den), u = cconj(v);
+        num = cmul(zi, qq);
+        den = csub(cscale(qq, float(N)), cmul(u, dq));
+    }
+    return cdiv(num, den);
+}
+
 template <int M>
 constexpr int wide_min_blocks() { return M <= 24 ? 3 : 2; }
 
@@ -99,7 +134,8 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
     constexpr int TW = (kBX + M - 1) | 1;        // odd float2 stride: conflict-free row-per-lane reads
     constexpr int TH = kBY + M - 1;
     __shared__ float2 tile[TH * TW];
-    __shared__ cx2 coef_s[kBY][N + 1];
+    __shared__ cx2 coef_s[kBY][64];              // P coefficients, zero-padded to 64 (lane-parallel polish)
+    __shared__ cx2 vec_s[kBY][2][64];            // per-warp broadcast vectors (u / q / roots, mirrors)
 
     const int lane = threadIdx.x, warp = threadIdx.y;
     const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
@@ -109,7 +145,17 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
     const bool rl = lane < M;
     const bool kl = lane < K;
     cx2* coef = coef_s[warp];
+    cx2* va = vec_s[warp][0];
+    cx2* vb = vec_s[warp][1];
     const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+    const cx2 kNegPos = cx2_make(-1.0f, 1.0f);
+    // zero padding: coef[N+1..63], va/vb[M..63] stay 0 (only indices < N+1 / < M are written)
+    for (int t = lane; t < 64; t += kBX) {
+        coef[t] = 0ull;
+        va[t] = 0ull;
+        vb[t] = 0ull;
+    }
+    __syncwarp();
 
     for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
         const float2* __restrict__ frame = frames + (size_t)f * plane;
@@ -191,13 +237,16 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     }
                     bool pow_ok = false;
                     for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                        if (rl) va[lane] = u;
+                        __syncwarp();
                         cx2 y = 0ull;
 #pragma unroll
                         for (int j = 0; j < M; ++j) {
-                            const cx2 uj = shfl_cx2(u, j);
-                            const cx2 ujj = mul2(cx2_make(cx2_im(uj), cx2_re(uj)), cx2_make(-1.0f, 1.0f));
+                            const cx2 uj = va[j];                                   // broadcast
+                            const cx2 ujj = mul2(cx2_make(cx2_im(uj), cx2_re(uj)), kNegPos);
                             y = fma2(cx2_bcast(cx2_re(R[j])), uj, fma2(cx2_bcast(cx2_im(R[j])), ujj, y));
                         }
+                        __syncwarp();
                         if (!rl) y = 0ull;
                         const float nrm2 = warp_sum(cabs2(cx2_f2(y)));
                         const cx2 yn = mul2(y, cx2_bcast(rsqrtf(nrm2)));
@@ -207,16 +256,19 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         if (diff < kPowerTol) { pow_ok = true; break; }
                     }
                     // v_1 ∝ Γ_w^H u_1, lane k holds v_k
+                    if (rl) va[lane] = u;
+                    __syncwarp();
                     cx2 v = 0ull;
 #pragma unroll
                     for (int i = 0; i < M; ++i) {
                         const float2 g = wrow[i * TW + p + ri];
-                        const cx2 ui = shfl_cx2(u, i);
+                        const cx2 ui = va[i];
                         const cx2 uinj = mul2(cx2_make(cx2_im(ui), cx2_re(ui)), kPosNeg);
                         v = fma2(cx2_bcast(g.x), ui, fma2(cx2_bcast(g.y), uinj, v));
                     }
                     if (!rl) v = 0ull;
                     v = mul2(v, cx2_bcast(rsqrtf(warp_sum(cabs2(cx2_f2(v))))));
+                    __syncwarp();
 
                     // ---- a4 + a5 per axis ----
                     float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
@@ -225,17 +277,17 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
 #pragma unroll 1
                     for (int axis = 0; axis < 2; ++axis) {
                         const cx2 q = axis ? v : u;
-                        const cx2 qnj = mul2(cx2_make(cx2_im(q), cx2_re(q)), kPosNeg);   // −j·q
+                        if (rl) va[lane] = q;                    // va[M..63] = 0
+                        __syncwarp();
                         // lane d: r_d = Σ_i q_i conj(q_{i+d}) = Σ_i re(q_{i+d})·q_i + im(q_{i+d})·(−j q_i)
                         const int d = lane;
                         cx2 r = 0ull;
 #pragma unroll
                         for (int i = 0; i < M - 1; ++i) {
-                            const cx2 qi = shfl_cx2(q, i), qinj = shfl_cx2(qnj, i);
-                            const cx2 qid = shfl_cx2(q, min(i + d, 31));
-                            const bool valid = d >= 1 && i + d < M;
-                            const cx2 t = fma2(cx2_bcast(cx2_re(qid)), qi, fma2(cx2_bcast(cx2_im(qid)), qinj, r));
-                            r = valid ? t : r;
+                            const cx2 qi = va[i];                                    // broadcast
+                            const cx2 qinj = mul2(cx2_make(cx2_im(qi), cx2_re(qi)), kPosNeg);   // −j·q_i
+                            const cx2 qid = va[i + d];                               // 0 beyond M
+                            r = fma2(cx2_bcast(cx2_re(qid)), qi, fma2(cx2_bcast(cx2_im(qid)), qinj, r));
                         }
                         const float n2 = warp_sum(cabs2(cx2_f2(q)));
                         const float2 rf = cx2_f2(r);
@@ -247,29 +299,33 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float2 r1q = cx2_f2(shfl_cx2(r, 1));
                         float2 rot = make_float2(1.0f, 0.0f);
                         if (cabs2(r1q) > 0.0f) rot = cscale(cconj(r1q), rsqrtf(cabs2(r1q)));
-                        __syncwarp();
+                        __syncwarp();                          // coef written, va free again
                         // Aberth–Ehrlich, lane k owns root k (simultaneous update)
                         float2 z = kl ? cmul(kTemplateRoots[bos_template_offset(M) + lane], rot) : make_float2(0.0f, 0.0f);
-                        cx2 zp = f2_cx2(z), zmp = kl ? mirror(zp) : 0ull;
+                        cx2 zp = f2_cx2(z);
                         int it = 0;
                         bool ok = false;
                         for (; it < kAberthMaxIt; ++it) {
+                            if (kl) {
+                                va[lane] = zp;
+                                vb[lane] = mirror(zp);
+                            }
+                            __syncwarp();
                             const float2 ratio = newton_ratio_smem<N>(coef, z);
                             const bool near = fabsf(1.0f - cabs2(z)) < kNearCircle;
                             const cx2 ziC = mul2(zp, kPosNeg);
-                            const cx2 kNegPos = cx2_make(-1.0f, 1.0f);
                             cx2 s = 0ull;
 #pragma unroll
                             for (int j = 0; j < K; ++j) {
-                                const cx2 zj = shfl_cx2(zp, j), zmj = shfl_cx2(zmp, j);
-                                const cx2 d1 = fma2(zj, kNegPos, ziC);
-                                const float q1 = fmaf(cx2_re(d1), cx2_re(d1), cx2_im(d1) * cx2_im(d1));
-                                const cx2 t1 = fma2(cx2_bcast(rcp_approx(q1)), d1, s);
-                                s = (j != lane) ? t1 : s;
-                                const cx2 d2 = fma2(zmj, kNegPos, ziC);
-                                const float q2 = fmaf(cx2_re(d2), cx2_re(d2), cx2_im(d2) * cx2_im(d2));
-                                const cx2 t2 = fma2(cx2_bcast(rcp_approx(q2)), d2, s);
-                                s = (j != lane || !near) ? t2 : s;
+                                // 1/(z − z_j) = conj(d)/|d|²; the own term gets |d|² = ∞ → 0
+                                const cx2 d1 = fma2(va[j], kNegPos, ziC);
+                                float q1 = fmaf(cx2_re(d1), cx2_re(d1), cx2_im(d1) * cx2_im(d1));
+                                q1 = (j == lane) ? CUDART_INF_F : q1;
+                                s = fma2(cx2_bcast(rcp_approx(q1)), d1, s);
+                                const cx2 d2 = fma2(vb[j], kNegPos, ziC);
+                                float q2 = fmaf(cx2_re(d2), cx2_re(d2), cx2_im(d2) * cx2_im(d2));
+                                q2 = (j == lane && near) ? CUDART_INF_F : q2;
+                                s = fma2(cx2_bcast(rcp_approx(q2)), d2, s);
                             }
                             const float2 sf = cx2_f2(s);
                             const float2 dd = make_float2(1.0f - (ratio.x * sf.x - ratio.y * sf.y),
@@ -283,7 +339,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             }
                             z = csub(z, w);
                             zp = f2_cx2(z);
-                            zmp = kl ? mirror(zp) : 0ull;
+                            __syncwarp();                      // everyone has read va/vb
                             if (warp_max(w2) < kAberthTol2) { ok = true; ++it; break; }
                         }
                         // selection: argmin |log2 |z|²| over lanes, margin to a different frequency
@@ -300,7 +356,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float marg = (second - best) * 0.34657359f;
 #pragma unroll 1
                         for (int t = 0; t < kPolishMax; ++t) {   // warp-uniform: zb is the same on all lanes
-                            const float2 wp = newton_ratio_smem<N>(coef, zb);
+                            const float2 wp = newton_ratio_warp<N>(coef, zb, lane);
                             const float w2 = cabs2(wp);
                             if (w2 < 1e30f) zb = csub(zb, wp);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;

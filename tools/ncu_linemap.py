@@ -1,6 +1,6 @@
 import re, csv, sys, subprocess, collections
 dis, rep, kern = sys.argv[1], sys.argv[2], sys.argv[3]
-src = open('/root/repo/paper_1910_11872_b200/csrc/demod_kernel.cuh').read().splitlines()
+import os; src = open(os.environ.get('SRC','/root/repo/paper_1910_11872_b200/csrc/demod_kernel.cuh')).read().splitlines()
 # parse disassembly of the kernel
 lines = open(dis).read().splitlines()
 start = None
@@ -32,7 +32,7 @@ for r in data:
     ex = int(r[ix['Thread Instructions Executed']] or 0)
     tot += ex
     ch = addr2.get(a, ([], ''))[0]
-    kl = [ln for f, ln in ch if f.endswith('demod_kernel.cuh')]
+    kl = [ln for f, ln in ch if f.endswith(os.path.basename(os.environ.get('SRC','demod_kernel.cuh')))]
     outer = kl[-1] if kl else -1
     by_outer[outer] += ex
     # second level: first kernel-file line in the chain that is > 80 (inside a device function body)
