@@ -57,7 +57,7 @@ enum : uint8_t {
 // squared step ratio ≈ (λ2/λ1)²) the remaining error² is ≈ diff_k·ρ²/(1−ρ)²; trust the
 // estimate only for a clear contraction (ρ² < 1/4, so (1−ρ)² ≥ 1/4).
 __device__ __forceinline__ bool power_converged(float diff, float prev_diff) {
-    return prev_diff < 1e30f && diff < 0.25f * prev_diff && diff * diff < 0.25f * kPowerPredTol * prev_diff;
+    return diff < 0.25f * prev_diff && diff * diff < 0.25f * kPowerPredTol * prev_diff;
 }
 
 // ---------------------------------------------------------------- complex helpers (FP32)
