@@ -34,7 +34,6 @@ constexpr int kThreads = kBX * kBY;
 
 constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyond)
 constexpr float kPowerTol = 1e-10f;   // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2))
-constexpr float kPowerPredTol = 1e-10f;  // predicted remaining ‖u − u_1‖² stop (see power_converged)
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.032), then polish
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
@@ -52,13 +51,6 @@ enum : uint8_t {
     kFlagNonfinite = 1u << 4,
     kFlagBorder = 1u << 5,
 };
-
-// Power-iteration stop from the observed contraction: with ρ² = diff_k/diff_{k−1} (the
-// squared step ratio ≈ (λ2/λ1)²) the remaining error² is ≈ diff_k·ρ²/(1−ρ)²; trust the
-// estimate only for a clear contraction (ρ² < 1/4, so (1−ρ)² ≥ 1/4).
-__device__ __forceinline__ bool power_converged(float diff, float prev_diff) {
-    return diff < 0.25f * prev_diff && diff * diff < 0.25f * kPowerPredTol * prev_diff;
-}
 
 // ---------------------------------------------------------------- complex helpers (FP32)
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -380,7 +372,6 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     }
                 }
                 bool pow_ok = false;
-                float prev_diff = CUDART_INF_F;
                 for (n_pow = 0; n_pow < kPowerMaxIt;) {
                     // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
                     cx2 uj[M];
@@ -414,8 +405,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         u[i] = yn;
                     }
                     ++n_pow;
-                    if (diff < kPowerTol || power_converged(diff, prev_diff)) { pow_ok = true; break; }
-                    prev_diff = diff;
+                    if (diff < kPowerTol) { pow_ok = true; break; }
                 }
                 // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
                 cx2 unj[M];

@@ -236,7 +236,6 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         u = rl ? cx2_make(ul.x, ul.y) : 0ull;
                     }
                     bool pow_ok = false;
-                    float prev_diff = CUDART_INF_F;
                     for (n_pow = 0; n_pow < kPowerMaxIt;) {
                         if (rl) va[lane] = u;
                         __syncwarp();
@@ -254,8 +253,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float diff = warp_sum(cabs2(cx2_f2(sub2(yn, u))));
                         u = yn;
                         ++n_pow;
-                        if (diff < kPowerTol || power_converged(diff, prev_diff)) { pow_ok = true; break; }
-                        prev_diff = diff;
+                        if (diff < kPowerTol) { pow_ok = true; break; }
                     }
                     // v_1 ∝ Γ_w^H u_1, lane k holds v_k
                     if (rl) va[lane] = u;
