@@ -162,7 +162,7 @@ def run_reference(args, world, rank):
 
     w = synth.workload("C3", H=args.size, W=args.size, window_len=args.window_len)
     F = args.cpu_sample_frames
-    n_px = max(256, args.cpu_sample_px // 8)
+    n_px = max(256, args.cpu_sample_px)
     frames = synth.make_stack(w, frames=[0] + list(range(1, F + 1))).numpy()
     times = []
     threads = 1
