@@ -237,3 +237,30 @@ def test_wide_kernel_nonfinite_does_not_leak_along_the_segment(M):
     bad = (ofl & R.FLAG_NONFINITE) != 0
     assert np.all(np.isnan(g[bad])) and np.all(gfl[bad] & bosrm.FLAG_NONFINITE)
     assert_parity(g, o, ofl, f"wide NaN M={M}", max_excluded_frac=0.9)
+
+
+def test_64bit_offsets_stack_beyond_2p32_pixels():
+    """n_frames·H·W > 2^32 (C5-scale offsets on one GPU): 1025 frames of 2048² (4.3e9 px,
+    32 GiB of input).  The last frames' sampled pixels match the oracle."""
+    free, _ = torch.cuda.mem_get_info()
+    T, H, W = 1025, 2048, 2048
+    need = T * H * W * (8 + 4) + (4 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB free")
+    w = synth.workload("C4")
+    frames = torch.empty(T, H, W, dtype=torch.complex64, device=DEV)
+    ref_frame = synth.make_frame(w, 0, device=DEV)
+    frames[:] = ref_frame                      # every frame = the reference ...
+    frames[T - 1] = synth.make_frame(w, 3, device=DEV)   # ... except the last one
+    out, _, ref = bosrm.bos_rootmusic_demod_stack(frames, 8, ref_index=0)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(64)
+    pix = (rng.integers(0, H, 2048), rng.integers(0, W, 2048))
+    host = torch.stack([frames[0], frames[T - 1]]).cpu().numpy()
+    o, ofl = R.demod_stack(host, 8, ref_index=0, pixels=pix, frame_indices=[1])
+    g = out[T - 1].cpu().numpy()[pix]
+    assert_parity(g, o[0], ofl[0], "frame 1024 of 1025 (offset > 2^32)")
+    mid = out[T // 2].cpu().numpy()
+    assert np.all(mid[np.isfinite(mid)] == 0.0)
+    del frames, out
+    torch.cuda.empty_cache()
