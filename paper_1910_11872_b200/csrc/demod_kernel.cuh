@@ -39,6 +39,7 @@ constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.0
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;
+constexpr float kRefineMargin = 0.05f; // selection margin (|ln|z||) below which the runner-up is polished too
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
@@ -217,7 +218,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
 // division; a root and its mirror tie, P:L208 [R6]) and the margin, in |ln|z|| units, to the
 // best root of a different frequency (|arg z − arg z_b| > τ_ω) for the AMBIGUOUS flag.
 template <int K>
-__device__ __forceinline__ float2 select_root(const cx2 (&zp)[K], float& margin) {
+__device__ __forceinline__ float2 select_root(const cx2 (&zp)[K], float& margin, float2& z2) {
     float best = CUDART_INF_F, rb2 = 1.0f;
     float2 zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
     float d[K];
@@ -229,16 +230,20 @@ __device__ __forceinline__ float2 select_root(const cx2 (&zp)[K], float& margin)
         if (d[i] < best) { best = d[i]; zb = z; rb2 = r2; }
     }
     float second = CUDART_INF_F;
+    z2 = zb;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         const float2 z = cx2_f2(zp[i]);
         const float dot = fmaf(z.x, zb.x, z.y * zb.y);        // Re(z_i conj(z_b)) = |z_i||z_b| cos Δ
         const bool distinct = dot < 0.0f || dot * dot < kCos2TauOmega * cabs2(z) * rb2;
-        if (distinct) second = fminf(second, d[i]);
+        if (distinct && d[i] < second) { second = d[i]; z2 = z; }
     }
     margin = (second - best) * 0.34657359f;                  // log2 → |ln r|: × ln2/2
     return zb;
 }
+
+// |ln|z|| of one root
+__device__ __forceinline__ float ln_dist(float2 z) { return 0.34657359f * fabsf(__log2f(cabs2(z))); }
 
 // Coefficients of P(z) = z^{M−1} q^H(z)(I − qq^H)q(z) for a unit vector q:
 // c_{M−1} = M − ‖q‖², c_{M−1+d} = −r_d, c_{M−1−d} = −conj(r_d), r_d = Σ_i q_i conj(q_{i+d}).
@@ -449,7 +454,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     bool ok;
                     const int its = aberth_sym<N>(c, z, ok);
                     float marg;
-                    float2 zs = select_root<N / 2>(z, marg);
+                    float2 z2;
+                    float2 zs = select_root<N / 2>(z, marg, z2);
                     // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
                     // ~1e-5 there); Newton steps on the selected root alone then make it
                     // FP32-accurate (quadratic) at 1/(M−1) of a sweep each.
@@ -459,6 +465,20 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float w2 = cabs2(w);
                         if (w2 < 1e30f) zs = csub(zs, w);
                         if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                    }
+                    // Near-tie between two frequencies: the loose sweeps may rank them wrongly, so
+                    // polish the runner-up too and re-select between the two converged roots.
+                    if (marg < kRefineMargin) {
+#pragma unroll 1
+                        for (int t = 0; t < kPolishMax; ++t) {
+                            const float2 w = newton_ratio<N>(c, z2);
+                            const float w2 = cabs2(w);
+                            if (w2 < 1e30f) z2 = csub(z2, w);
+                            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                        }
+                        const float d1 = ln_dist(zs), d2 = ln_dist(z2);
+                        if (d2 < d1) zs = z2;
+                        marg = fabsf(d2 - d1);
                     }
                     if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
                     else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }

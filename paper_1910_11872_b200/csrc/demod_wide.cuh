@@ -352,14 +352,29 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float rb2 = cabs2(zb);
                         const float dot = fmaf(z.x, zb.x, z.y * zb.y);
                         const bool distinct = kl && (dot < 0.0f || dot * dot < kCos2TauOmega * r2 * rb2);
-                        const float second = warp_min(distinct ? dl : CUDART_INF_F);
-                        const float marg = (second - best) * 0.34657359f;
+                        const float dd2 = distinct ? dl : CUDART_INF_F;
+                        const float second = warp_min(dd2);
+                        float marg = (second - best) * 0.34657359f;
+                        const int sl = __ffs(__ballot_sync(0xffffffffu, dd2 == second && second < CUDART_INF_F)) - 1;
+                        float2 z2 = cx2_f2(shfl_cx2(zp, sl < 0 ? 0 : sl));
 #pragma unroll 1
                         for (int t = 0; t < kPolishMax; ++t) {   // warp-uniform: zb is the same on all lanes
                             const float2 wp = newton_ratio_warp<N>(coef, zb, lane);
                             const float w2 = cabs2(wp);
                             if (w2 < 1e30f) zb = csub(zb, wp);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                        }
+                        if (marg < kRefineMargin && sl >= 0) {     // warp-uniform (see demod_kernel.cuh)
+#pragma unroll 1
+                            for (int t = 0; t < kPolishMax; ++t) {
+                                const float2 wp = newton_ratio_warp<N>(coef, z2, lane);
+                                const float w2 = cabs2(wp);
+                                if (w2 < 1e30f) z2 = csub(z2, wp);
+                                if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                            }
+                            const float d1 = ln_dist(zb), d2 = ln_dist(z2);
+                            if (d2 < d1) zb = z2;
+                            marg = fabsf(d2 - d1);
                         }
                         __syncwarp();                // coefficient buffer reused by the next axis
                         if (axis == 0) { zy = zb; my = marg; aby_ok = ok; n_aby = it; }

@@ -264,3 +264,19 @@ def test_64bit_offsets_stack_beyond_2p32_pixels():
     assert np.all(mid[np.isfinite(mid)] == 0.0)
     del frames, out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("M", [24, 32])
+def test_c4_large_windows_sampled_parity(M):
+    """C4 frames (2048², diffusion flow, 10 dB) at large windows: 2048 random pixels of frame 7,
+    plus the near-tie pixel (2, 255) where the runner-up root must be refined (M = 32)."""
+    w = synth.workload("C4")
+    frames = synth.make_stack(w, frames=[0, 7], device=DEV)
+    raw, _ = bosrm.bos_rootmusic_demod(frames, M)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(M)
+    py = np.concatenate([[2], rng.integers(0, w.H, 2047)])
+    px = np.concatenate([[255], rng.integers(0, w.W, 2047)])
+    host = frames.cpu().numpy()
+    o, ofl = R.demod_frame(host[1], M, pixels=(py, px))
+    assert_parity(raw[1].cpu().numpy()[py, px], o, ofl, f"C4 M={M}")
