@@ -40,6 +40,8 @@ constexpr int kPolishMin = 2;         // Newton steps on the selected root after
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;
 constexpr float kRefineMargin = 0.05f; // selection margin (|ln|z||) below which the runner-up is polished too
+constexpr float kMoved2 = 1e-4f;       // polish displacement² that triggers tight re-convergence
+constexpr float kAberthTightTol2 = 1e-10f;
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
@@ -151,7 +153,7 @@ __device__ __forceinline__ cx2 mirror(cx2 z) {
 // root update.  Complex values are packed (cx2.cuh): Horner and the reciprocal sum run on
 // FFMA2.  Returns the number of sweeps; `ok` = converged or stagnated at FP32 noise.
 template <int N>
-__device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2], bool& ok) {
+__device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2], bool& ok, float tol2) {
     constexpr int K = N / 2;
     cx2 zm[K];
 #pragma unroll
@@ -209,7 +211,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
             z[K - 1] = zn;
             zm[K - 1] = mirror(zn);
         }
-        if (maxw < kAberthTol2) { ok = true; ++it; break; }
+        if (maxw < tol2) { ok = true; ++it; break; }
     }
     return it;
 }
@@ -451,20 +453,34 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     cx2 z[N / 2];       // the inside half of the rotated template
 #pragma unroll
                     for (int j = 0; j < N / 2; ++j) z[j] = f2_cx2(cmul(kTemplateRoots[bos_template_offset(M) + j], rot));
-                    bool ok;
-                    const int its = aberth_sym<N>(c, z, ok);
-                    float marg;
-                    float2 z2;
-                    float2 zs = select_root<N / 2>(z, marg, z2);
-                    // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
-                    // ~1e-5 there); Newton steps on the selected root alone then make it
-                    // FP32-accurate (quadratic) at 1/(M−1) of a sweep each.
+                    bool ok = false;
+                    int its = 0;
+                    float marg = CUDART_INF_F;
+                    float2 zs, z2;
+                    float tol2 = kAberthTol2;
 #pragma unroll 1
-                    for (int t = 0; t < kPolishMax; ++t) {
-                        const float2 w = newton_ratio<N>(c, zs);
-                        const float w2 = cabs2(w);
-                        if (w2 < 1e30f) zs = csub(zs, w);
-                        if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                    for (int attempt = 0;; ++attempt) {
+                        its += aberth_sym<N>(c, z, ok, tol2);
+                        zs = select_root<N / 2>(z, marg, z2);
+                        // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
+                        // ~1e-5 there); Newton steps on the selected root alone then make it
+                        // FP32-accurate (quadratic) at 1/(M−1) of a sweep each.
+                        const float2 zsel = zs;
+#pragma unroll 1
+                        for (int t = 0; t < kPolishMax; ++t) {
+                            const float2 w = newton_ratio<N>(c, zs);
+                            const float w2 = cabs2(w);
+                            if (w2 < 1e30f) zs = csub(zs, w);
+                            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                        }
+                        // A selected approximation that the polish moves far was not near a root
+                        // (loose sweeps can park an approximation between roots): converge all
+                        // roots tightly and select again.
+                        if (attempt == 0 && !(cabs2(csub(zs, zsel)) <= kMoved2)) {
+                            tol2 = kAberthTightTol2;
+                            continue;
+                        }
+                        break;
                     }
                     // Near-tie between two frequencies: the loose sweeps may rank them wrongly, so
                     // polish the runner-up too and re-select between the two converged roots.

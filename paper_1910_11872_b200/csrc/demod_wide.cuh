@@ -305,7 +305,13 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         cx2 zp = f2_cx2(z);
                         int it = 0;
                         bool ok = false;
-                        for (; it < kAberthMaxIt; ++it) {
+                        float tol2 = kAberthTol2;
+                        float2 zb, z2;
+                        float marg;
+                        int sl;
+#pragma unroll 1
+                        for (int attempt = 0;; ++attempt) {      // warp-uniform (see demod_kernel.cuh)
+                        for (int sweep = 0; sweep < kAberthMaxIt; ++sweep, ++it) {
                             if (kl) {
                                 va[lane] = zp;
                                 vb[lane] = mirror(zp);
@@ -340,29 +346,36 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             z = csub(z, w);
                             zp = f2_cx2(z);
                             __syncwarp();                      // everyone has read va/vb
-                            if (warp_max(w2) < kAberthTol2) { ok = true; ++it; break; }
+                            if (warp_max(w2) < tol2) { ok = true; ++it; break; }
                         }
                         // selection: argmin |log2 |z|²| over lanes, margin to a different frequency
                         const float r2 = cabs2(z);
                         const float dl = kl ? fabsf(__log2f(r2)) : CUDART_INF_F;
                         const float best = warp_min(dl);
                         const int bl = __ffs(__ballot_sync(0xffffffffu, dl == best)) - 1;
-                        float2 zb = cx2_f2(shfl_cx2(zp, bl < 0 ? 0 : bl));
+                        zb = cx2_f2(shfl_cx2(zp, bl < 0 ? 0 : bl));
                         if (!(best < CUDART_INF_F)) zb = make_float2(CUDART_NAN_F, CUDART_NAN_F);
                         const float rb2 = cabs2(zb);
                         const float dot = fmaf(z.x, zb.x, z.y * zb.y);
                         const bool distinct = kl && (dot < 0.0f || dot * dot < kCos2TauOmega * r2 * rb2);
                         const float dd2 = distinct ? dl : CUDART_INF_F;
                         const float second = warp_min(dd2);
-                        float marg = (second - best) * 0.34657359f;
-                        const int sl = __ffs(__ballot_sync(0xffffffffu, dd2 == second && second < CUDART_INF_F)) - 1;
-                        float2 z2 = cx2_f2(shfl_cx2(zp, sl < 0 ? 0 : sl));
+                        marg = (second - best) * 0.34657359f;
+                        sl = __ffs(__ballot_sync(0xffffffffu, dd2 == second && second < CUDART_INF_F)) - 1;
+                        z2 = cx2_f2(shfl_cx2(zp, sl < 0 ? 0 : sl));
+                        const float2 zsel = zb;
 #pragma unroll 1
                         for (int t = 0; t < kPolishMax; ++t) {   // warp-uniform: zb is the same on all lanes
                             const float2 wp = newton_ratio_warp<N>(coef, zb, lane);
                             const float w2 = cabs2(wp);
                             if (w2 < 1e30f) zb = csub(zb, wp);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                        }
+                        if (attempt == 0 && !(cabs2(csub(zb, zsel)) <= kMoved2)) {
+                            tol2 = kAberthTightTol2;
+                            continue;
+                        }
+                        break;
                         }
                         if (marg < kRefineMargin && sl >= 0) {     // warp-uniform (see demod_kernel.cuh)
 #pragma unroll 1
