@@ -134,6 +134,13 @@ __device__ __forceinline__ float2 newton_on_derivative(const cx2 (&c)[N + 1], fl
     return cdiv(cx2_f2(dp), cscale(cx2_f2(ddp), 2.0f));
 }
 
+// One polish step on a single root, consistent with the sweeps: Newton on P, or on P′ for a
+// root in the near-circle band (a near-double pair, whose centre carries the pair's arg).
+template <int N>
+__device__ __forceinline__ float2 polish_step(const cx2 (&c)[N + 1], float2 z) {
+    return fabsf(1.0f - cabs2(z)) < kNearCircle ? newton_on_derivative<N>(c, z) : newton_ratio<N>(c, z);
+}
+
 // 1/|z|² · z = 1/z̄ (the mirror of z through the unit circle)
 __device__ __forceinline__ cx2 mirror(cx2 z) {
     const float re = cx2_re(z), im = cx2_im(z);
@@ -468,7 +475,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float2 zsel = zs;
 #pragma unroll 1
                         for (int t = 0; t < kPolishMax; ++t) {
-                            const float2 w = newton_ratio<N>(c, zs);
+                            const float2 w = polish_step<N>(c, zs);
                             const float w2 = cabs2(w);
                             if (w2 < 1e30f) zs = csub(zs, w);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
@@ -487,7 +494,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     if (marg < kRefineMargin) {
 #pragma unroll 1
                         for (int t = 0; t < kPolishMax; ++t) {
-                            const float2 w = newton_ratio<N>(c, z2);
+                            const float2 w = polish_step<N>(c, z2);
                             const float w2 = cabs2(w);
                             if (w2 < 1e30f) z2 = csub(z2, w);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;

@@ -91,10 +91,11 @@ __device__ __forceinline__ float2 newton_on_derivative_smem(const cx2* __restric
 template <int N>
 __device__ __forceinline__ float2 newton_ratio_warp(const cx2* __restrict__ c, float2 zi, int lane) {
     const float m2 = cabs2(zi);
-    const bool outside = m2 > 1.0f;
+    const bool near = fabsf(1.0f - m2) < kNearCircle;    // near-double pair: Newton on P′ (see polish_step)
+    const bool outside = !near && m2 > 1.0f;
     const float2 v = outside ? cscale(zi, __fdividef(1.0f, m2)) : zi;
     const float2 v2 = cmul(v, v);
-    // q = (v²)^{l−1} for l ≥ 1 (5-bit exponent)
+    // q = (v²)^{l−1} = v^{2l−2} for l ≥ 1 (5-bit exponent)
     const int e = lane > 0 ? lane - 1 : 0;
     float2 q = make_float2(1.0f, 0.0f), b = v2;
 #pragma unroll
@@ -105,16 +106,25 @@ __device__ __forceinline__ float2 newton_ratio_warp(const cx2* __restrict__ c, f
     const float2 pm1 = cmul(q, v);                                  // v^{2l−1}
     const float2 pw = lane > 0 ? cmul(pm1, v) : make_float2(1.0f, 0.0f);   // v^{2l}
     const float2 c0 = cx2_f2(c[2 * lane]), c1 = cx2_f2(c[2 * lane + 1]);
-    const float2 pp = cmul(pw, cfma(c1, v, c0));                    // c0 v^{2l} + c1 v^{2l+1}
     const float a = float(2 * lane);
-    const float2 dterm = cfma(cscale(c1, a + 1.0f), v, cscale(c0, a));   // 2l·c0 + (2l+1)·c1·v
-    const float2 dd = lane > 0 ? cmul(pm1, dterm) : c1;              // d/dv of the two terms
-    const float2 P = warp_sum2(pp), D = warp_sum2(dd);
-    float2 num = P, den = D;
-    if (outside) {
-        const float2 qq = cconj(num), dq = cconj(den), u = cconj(v);
-        num = cmul(zi, qq);
-        den = csub(cscale(qq, float(N)), cmul(u, dq));
+    // terms k = 2l, 2l+1 of P, P′ and P″
+    const float2 pp = cmul(pw, cfma(c1, v, c0));
+    const float2 dterm = cfma(cscale(c1, a + 1.0f), v, cscale(c0, a));          // 2l·c0 + (2l+1)·c1·v
+    const float2 dd = lane > 0 ? cmul(pm1, dterm) : c1;
+    float2 num, den;
+    if (near) {                                                          // warp-uniform (zi is)
+        const float2 d2term = cfma(cscale(c1, (a + 1.0f) * a), v, cscale(c0, a * (a - 1.0f)));
+        const float2 dd2 = lane > 0 ? cmul(q, d2term) : make_float2(0.0f, 0.0f);
+        num = warp_sum2(dd);
+        den = warp_sum2(dd2);
+    } else {
+        num = warp_sum2(pp);
+        den = warp_sum2(dd);
+        if (outside) {
+            const float2 qq = cconj(num), dq = cconj(den), u = cconj(v);
+            num = cmul(zi, qq);
+            den = csub(cscale(qq, float(N)), cmul(u, dq));
+        }
     }
     return cdiv(num, den);
 }
