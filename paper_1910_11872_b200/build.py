@@ -56,10 +56,16 @@ def _run(cmd, log):
     return p.stdout
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
-    """Compile (if sources changed) and return the path of libbosrm.so."""
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile (if sources changed) and return the path of libbosrm.so.
+    `defines` / `out` build a variant library (development A/B builds)."""
+    global BUILD, LIB
+    if out is not None:
+        BUILD = os.path.join(ROOT, "build", os.path.splitext(os.path.basename(out))[0])
+        LIB = out
     os.makedirs(BUILD, exist_ok=True)
-    digest = _sources_digest([])
+    extra = [f"-D{d}" for d in defines]
+    digest = _sources_digest(extra)
     stamp = os.path.join(BUILD, "stamp")
     if not force and os.path.exists(LIB) and os.path.exists(stamp):
         with open(stamp) as fh:
@@ -69,13 +75,13 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     jobs = jobs or max(1, min(len(WINDOW_LENS) + 1, os.cpu_count() or 1))
     tasks = []
     host_obj = os.path.join(BUILD, "bos_rootmusic.o")
-    tasks.append(([cc, *NVFLAGS, "-c", os.path.join(CSRC, "bos_rootmusic.cu"), "-o", host_obj],
+    tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, "bos_rootmusic.cu"), "-o", host_obj],
                   host_obj + ".log"))
     objs = [host_obj]
     for M in WINDOW_LENS:
         o = os.path.join(BUILD, f"demod_m{M}.o")
         objs.append(o)
-        tasks.append(([cc, *NVFLAGS, f"-DBOS_INST_M={M}", "-c", os.path.join(CSRC, "demod_inst.cu"), "-o", o],
+        tasks.append(([cc, *NVFLAGS, *extra, f"-DBOS_INST_M={M}", "-c", os.path.join(CSRC, "demod_inst.cu"), "-o", o],
                       o + ".log"))
     # longest (largest M) first
     tasks = [tasks[0]] + tasks[1:][::-1]
