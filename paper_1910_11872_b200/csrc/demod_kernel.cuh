@@ -182,11 +182,11 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
             const bool near = fabsf(1.0f - cabs2(zi)) < kNearCircle;
             // s = Σ 1/(z_i − z_j) = Σ conj(d)/|d|², d = z_i − z_j; conj(d) = conj(z_i) + (−1,1)⊙z_j
             const cx2 ziC = mul2(z[0], cx2_make(1.0f, -1.0f));
-            cx2 s = 0ull;
+            cx2 s = 0ull, sm = 0ull;           // two accumulators: halves the FFMA2 dependency chain
             {
                 const cx2 dc = fma2(zm[0], kNegPos, ziC);
                 const float q = fmaf(cx2_re(dc), cx2_re(dc), cx2_im(dc) * cx2_im(dc));
-                s = near ? 0ull : mul2(cx2_bcast(rcp_approx(q)), dc);
+                sm = near ? 0ull : mul2(cx2_bcast(rcp_approx(q)), dc);
             }
 #pragma unroll
             for (int j = 1; j < K; ++j) {
@@ -195,9 +195,9 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
                 s = fma2(cx2_bcast(rcp_approx(q1)), d1, s);
                 const cx2 d2 = fma2(zm[j], kNegPos, ziC);
                 const float q2 = fmaf(cx2_re(d2), cx2_re(d2), cx2_im(d2) * cx2_im(d2));
-                s = fma2(cx2_bcast(rcp_approx(q2)), d2, s);
+                sm = fma2(cx2_bcast(rcp_approx(q2)), d2, sm);
             }
-            const float2 sf = cx2_f2(s);
+            const float2 sf = cx2_f2(add2(s, sm));
             // Aberth correction w = ratio / (1 − ratio·s)
             const float2 d1 = make_float2(1.0f - (ratio.x * sf.x - ratio.y * sf.y),
                                           -(ratio.x * sf.y + ratio.y * sf.x));
