@@ -129,30 +129,6 @@ __device__ __forceinline__ float2 newton_ratio_warp(const cx2* __restrict__ c, f
     return cdiv(num, den);
 }
 
-// One Aberth step for a single root zb (lane `self` tracks it) against the other roots held
-// one per lane (z) and their mirrors: w = N/(1 − N·S), S = Σ_{j≠self} 1/(zb − z_j) +
-// Σ_j 1/(zb − 1/z̄_j) (own mirror only outside the near band), warp-reduced.  Cubic instead of
-// Newton's quadratic convergence from the loosely converged sweep; near the circle it is the
-// Newton-on-P′ step of newton_ratio_warp.
-template <int N>
-__device__ __forceinline__ float2 aberth_polish_warp(const cx2* __restrict__ c, float2 zb, float2 z, int self,
-                                                     int lane, bool kl) {
-    const float2 ratio = newton_ratio_warp<N>(c, zb, lane);
-    const bool near = fabsf(1.0f - cabs2(zb)) < kNearCircle;       // warp-uniform
-    if (near) return ratio;                                           // already P′/P″
-    float2 t = make_float2(0.0f, 0.0f);
-    if (kl) {
-        const float2 zo = lane == self ? zb : z;                      // own mirror: of zb itself
-        const float2 zm = cscale(zo, __fdividef(1.0f, cabs2(zo)));
-        const float2 d2 = csub(zb, zm);
-        t = crcp(d2);
-        if (lane != self) t = cadd(t, crcp(csub(zb, z)));
-    }
-    const float2 sf = warp_sum2(t);
-    const float2 dd = make_float2(1.0f - (ratio.x * sf.x - ratio.y * sf.y), -(ratio.x * sf.y + ratio.y * sf.x));
-    return cdiv(ratio, dd);
-}
-
 template <int M>
 constexpr int wide_min_blocks() { return M <= 24 ? 3 : 2; }
 
@@ -400,7 +376,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         const float2 zsel = zb;
 #pragma unroll 1
                         for (int t = 0; t < kPolishMax; ++t) {   // warp-uniform: zb is the same on all lanes
-                            const float2 wp = aberth_polish_warp<N>(coef, zb, z, bl, lane, kl);
+                            const float2 wp = newton_ratio_warp<N>(coef, zb, lane);
                             const float w2 = cabs2(wp);
                             if (w2 < 1e30f) zb = csub(zb, wp);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
@@ -414,7 +390,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         if (marg < kRefineMargin && sl >= 0) {     // warp-uniform (see demod_kernel.cuh)
 #pragma unroll 1
                             for (int t = 0; t < kPolishMax; ++t) {
-                                const float2 wp = aberth_polish_warp<N>(coef, z2, z, sl, lane, kl);
+                                const float2 wp = newton_ratio_warp<N>(coef, z2, lane);
                                 const float w2 = cabs2(wp);
                                 if (w2 < 1e30f) z2 = csub(z2, wp);
                                 if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
