@@ -131,6 +131,34 @@ int bos_rootmusic_demod_stack_host(const bos_cf32* h_frames, int n_frames, int H
                                    int chunk_frames, void* stream);
 
 /*
+ * bos_rootmusic_demod_ex — bos_rootmusic_demod that also writes the local fringe
+ * frequencies of Eq.(15): ω_y = arg z_y and ω_x = −arg z_x, rad/pixel in
+ * (−π, π].
+ *   omega_x, omega_y  DEVICE [n_frames][H][W] float32 each, or NULL (not written); must not
+ *                     overlap frames, out_phase or each other.  NaN where the window is
+ *                     non-finite.
+ * Other arguments, errors and determinism as bos_rootmusic_demod.
+ */
+int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W,
+                           int window_len, int model_order, const float* ref_phase,
+                           float* out_phase, uint8_t* flags, float* omega_x, float* omega_y,
+                           void* stream);
+
+/*
+ * bos_index_gradient — Eq.(17): the refractive-index derivative is
+ * proportional to the (unwrapped) phase,  ∂n/∂x = (1/(2 μ f_x)) · (n0 / L²) · φ.
+ *   phase   DEVICE float32 [n] (a phase map/stack; unwrapping is the caller's).
+ *   n0      reference refractive index (> 0); mu: the μ of Eq.(17) (> 0, read as the imaging
+ *           magnification); f_x: fringe frequency (> 0, cycles per unit length);
+ *           cell_len: test-cell length L along the optical axis (> 0).  Consistent units in
+ *           (e.g. SI) give ∂n/∂x in the same system (1/m for SI).
+ *   out     DEVICE float32 [n]; may equal `phase` (in place), must not partially overlap it.
+ * Returns BOS_ERR_INVALID_ARG for NULL/host pointers, n == 0 or non-positive parameters.
+ */
+int bos_index_gradient(const float* phase, size_t n, double n0, double mu, double f_x,
+                       double cell_len, float* out, void* stream);
+
+/*
  * bos_rootmusic_iteration_counts — measurement support for the roofline:
  * runs the same kernel with per-pixel iteration counters over `frames` (DEVICE, as in
  * bos_rootmusic_demod) and accumulates into d_counters (DEVICE, 4 × uint64, caller zeroes):

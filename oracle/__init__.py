@@ -19,6 +19,7 @@ from .rootmusic import (  # noqa: F401
     demod_stack,
     estimate_windows,
     extract_windows,
+    index_gradient,
     music_polynomial,
     noise_projectors,
     select_root,

@@ -340,3 +340,8 @@ def rms_max_wrapped(a, b, valid=None):
     if e.size == 0:
         return 0.0, 0.0, 0
     return float(math.sqrt(np.mean(e * e))), float(np.max(np.abs(e))), int(e.size)
+
+
+def index_gradient(phase, n0: float, mu: float, f_x: float, cell_len: float):
+    """Eq.(17): ∂n/∂x = (1/(2 μ f_x)) · (n0 / L²) · φ, pointwise (FP64)."""
+    return (1.0 / (2.0 * mu * f_x)) * (n0 / (cell_len * cell_len)) * np.asarray(phase, dtype=np.float64)

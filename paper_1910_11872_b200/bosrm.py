@@ -40,6 +40,9 @@ SIGNATURES = {
     "bos_rootmusic_host_workspace_bytes": (_SZ, [_I, _I, _I, _I]),
     "bos_rootmusic_demod_stack_host": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _SZ, _I, _VP]),
     "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
+    "bos_rootmusic_demod_ex": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "bos_index_gradient": (_I, [_VP, _SZ, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                _VP, _VP]),
     "bos_strerror": (ctypes.c_char_p, [_I]),
     "bos_abi_version": (_I, []),
 }
@@ -208,3 +211,37 @@ def bos_rootmusic_iteration_counts(frames: torch.Tensor, window_len: int = 8, mo
     _check(rc, "bos_rootmusic_iteration_counts")
     c = cnt.cpu().tolist()
     return dict(pixels=c[0], power_its=c[1], aberth_y=c[2], aberth_x=c[3], out=out)
+
+
+def bos_rootmusic_demod_ex(frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
+                           ref_phase: torch.Tensor | None = None, flags=None, omega=True, stream=None):
+    """bos_rootmusic_demod plus the Eq.(15) local frequency maps → (phase, flags|None, ω_x, ω_y)."""
+    frames = _dev_tensor(_frames3(frames), torch.complex64, "frames")
+    T, H, W = frames.shape
+    dev = frames.device
+    out = torch.empty(T, H, W, dtype=torch.float32, device=dev)
+    fl = torch.empty(T, H, W, dtype=torch.uint8, device=dev) if flags else None
+    wx = torch.empty(T, H, W, dtype=torch.float32, device=dev) if omega else None
+    wy = torch.empty(T, H, W, dtype=torch.float32, device=dev) if omega else None
+    if ref_phase is not None:
+        _dev_tensor(ref_phase, torch.float32, "ref_phase")
+    rc = lib().bos_rootmusic_demod_ex(
+        frames.data_ptr(), T, H, W, int(window_len), int(model_order),
+        ref_phase.data_ptr() if ref_phase is not None else None, out.data_ptr(),
+        fl.data_ptr() if fl is not None else None, wx.data_ptr() if wx is not None else None,
+        wy.data_ptr() if wy is not None else None, _stream_ptr(stream))
+    _check(rc, "bos_rootmusic_demod_ex")
+    return out, fl, wx, wy
+
+
+def bos_index_gradient(phase: torch.Tensor, n0: float, mu: float, f_x: float, cell_len: float,
+                       out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Eq.(17): ∂n/∂x = n0 / (2 μ f_x L²) · φ on a CUDA float32 tensor (any shape)."""
+    _dev_tensor(phase, torch.float32, "phase")
+    if out is None:
+        out = torch.empty_like(phase)
+    _dev_tensor(out, torch.float32, "out")
+    rc = lib().bos_index_gradient(phase.data_ptr(), phase.numel(), float(n0), float(mu), float(f_x),
+                                  float(cell_len), out.data_ptr(), _stream_ptr(stream))
+    _check(rc, "bos_index_gradient")
+    return out

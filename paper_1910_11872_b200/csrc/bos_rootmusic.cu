@@ -12,7 +12,7 @@
 
 namespace {
 
-using LaunchFn = cudaError_t (*)(const float2*, int, int, int, const float*, float*, uint8_t*,
+using LaunchFn = cudaError_t (*)(const float2*, int, int, int, const float*, float*, uint8_t*, float*, float*,
                                  unsigned long long*, cudaStream_t);
 
 template <bool COUNT>
@@ -78,7 +78,7 @@ int check_common(int n_frames, int H, int W, int window_len, int model_order) {
 
 int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_len, int model_order,
                const float* ref_phase, float* out_phase, uint8_t* flags, unsigned long long* counters,
-               void* stream, bool check_ptrs) {
+               void* stream, bool check_ptrs, float* omega_x = nullptr, float* omega_y = nullptr) {
     int rc = check_common(n_frames, H, W, window_len, model_order);
     if (rc != BOS_OK) return rc;
     if (frames == nullptr || out_phase == nullptr) return BOS_ERR_INVALID_ARG;
@@ -90,6 +90,14 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
     if (flags != nullptr && (overlaps(flags, n, out_phase, n * sizeof(float)) ||
                              overlaps(flags, n, frames, n * sizeof(bos_cf32))))
         return BOS_ERR_INVALID_ARG;
+    for (float* om : {omega_x, omega_y}) {
+        if (om == nullptr) continue;
+        if (overlaps(om, n * sizeof(float), out_phase, n * sizeof(float)) ||
+            overlaps(om, n * sizeof(float), frames, n * sizeof(bos_cf32)))
+            return BOS_ERR_INVALID_ARG;
+        if (check_ptrs && !is_device_ptr(om)) return BOS_ERR_INVALID_ARG;
+    }
+    if (omega_x != nullptr && omega_x == omega_y) return BOS_ERR_INVALID_ARG;
     if (check_ptrs) {
         if (!is_device_ptr(frames) || !is_device_ptr(out_phase)) return BOS_ERR_INVALID_ARG;
         if (ref_phase != nullptr && !is_device_ptr(ref_phase)) return BOS_ERR_INVALID_ARG;
@@ -98,11 +106,31 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
     LaunchFn fn = counters ? pick<true>(window_len) : pick<false>(window_len);
     if (fn == nullptr) return BOS_ERR_UNSUPPORTED;
     const cudaError_t e = fn(reinterpret_cast<const float2*>(frames), n_frames, H, W, ref_phase, out_phase,
-                             flags, counters, static_cast<cudaStream_t>(stream));
+                             flags, omega_x, omega_y, counters, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// Eq.(17): ∂n/∂x = (1/(2 μ f_x)) (n0/L²) φ — a pointwise scale (vectorised, HBM-bound).
+__global__ void index_gradient_kernel(const float* __restrict__ phase, size_t n, float k, float* __restrict__ out) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t n4 = n / 4;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(phase) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (aligned) {
+        const float4* p4 = reinterpret_cast<const float4*>(phase);
+        float4* o4 = reinterpret_cast<float4*>(out);
+        for (size_t j = i; j < n4; j += stride) {
+            float4 v = __ldg(p4 + j);
+            v.x *= k; v.y *= k; v.z *= k; v.w *= k;
+            o4[j] = v;
+        }
+        for (size_t j = 4 * n4 + i; j < n; j += stride) out[j] = k * phase[j];
+    } else {
+        for (size_t j = i; j < n; j += stride) out[j] = k * phase[j];
+    }
+}
 
 }  // namespace
 
@@ -124,6 +152,25 @@ int bos_rootmusic_demod(const bos_cf32* frames, int n_frames, int H, int W, int 
                         const float* ref_phase, float* out_phase, uint8_t* flags, void* stream) {
     return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, flags, nullptr,
                       stream, true);
+}
+
+int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W, int window_len, int model_order,
+                           const float* ref_phase, float* out_phase, uint8_t* flags, float* omega_x, float* omega_y,
+                           void* stream) {
+    return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, flags, nullptr,
+                      stream, true, omega_x, omega_y);
+}
+
+int bos_index_gradient(const float* phase, size_t n, double n0, double mu, double f_x, double cell_len,
+                       float* out, void* stream) {
+    if (phase == nullptr || out == nullptr || n == 0) return BOS_ERR_INVALID_ARG;
+    if (!(mu > 0.0) || !(f_x > 0.0) || !(cell_len > 0.0) || !(n0 > 0.0)) return BOS_ERR_INVALID_ARG;
+    if (phase != out && overlaps(phase, n * sizeof(float), out, n * sizeof(float))) return BOS_ERR_INVALID_ARG;
+    if (!is_device_ptr(phase) || !is_device_ptr(out)) return BOS_ERR_INVALID_ARG;
+    const double k = n0 / (2.0 * mu * f_x * cell_len * cell_len);
+    const unsigned blocks = (unsigned)std::min<size_t>((n / 4 + 255) / 256 + 1, 148 * 16);
+    index_gradient_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(phase, n, (float)k, out);
+    return cudaGetLastError() == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 
 int bos_rootmusic_iteration_counts(const bos_cf32* frames, int n_frames, int H, int W, int window_len,

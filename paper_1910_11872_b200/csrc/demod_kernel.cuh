@@ -296,7 +296,7 @@ template <int M, bool COUNT>
 __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<M>())
 demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
              const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
-             unsigned long long* __restrict__ counters) {
+             float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
     constexpr int N = 2 * M - 2;                 // polynomial degree
     constexpr int O0 = (M - 1) / 2;              // o_i = i − O0  [R2]
     constexpr int TW = kBX + M - 1;
@@ -363,7 +363,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
 #pragma unroll
             for (int i = 0; i < M; ++i) trace += Rd[i];
 
-            float result;
+            float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
             int n_pow = 0, n_aby = 0, n_abx = 0;
             if (!isfinite(trace)) {
                 fl |= kFlagNonfinite;
@@ -545,6 +545,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 if (!(cabs2(csum) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
                 float a = atan2f(csum.y, csum.x);
                 // ---- a7: reference difference, wrap into (−π, π] ----
+                if (omx != nullptr) wx = -atan2f(zx.y, zx.x);       // Eq.(15): ω_x = −arg z_x
+                if (omy != nullptr) wy = atan2f(zy.y, zy.x);        //          ω_y =  arg z_y
                 if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
                 if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
                 if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
@@ -553,6 +555,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
             const size_t o = (size_t)f * plane + (size_t)py * W + px;
             out[o] = result;
             if (flags != nullptr) flags[o] = fl;
+            if (omx != nullptr) omx[o] = wx;
+            if (omy != nullptr) omy[o] = wy;
             if (COUNT) {
                 atomicAdd(counters + 0, 1ull);
                 atomicAdd(counters + 1, (unsigned long long)n_pow);

@@ -136,7 +136,7 @@ template <int M, bool COUNT>
 __global__ void __launch_bounds__(kThreads, wide_min_blocks<M>())
 demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                   const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
-                  unsigned long long* __restrict__ counters) {
+                  float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
     static_assert(M >= kWideMinM && M <= 32, "wide kernel: 17 <= M <= 32");
     constexpr int N = 2 * M - 2;                 // polynomial degree
     constexpr int K = N / 2;                     // tracked (inside) roots, one per lane
@@ -224,7 +224,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 uint8_t fl = 0;
                 if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
                     fl |= kFlagBorder;
-                float result;
+                float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
                 int n_pow = 0, n_aby = 0, n_abx = 0;
                 rebuild = !isfinite(trace);          // NaN/Inf never leave R by subtraction
                 if (!isfinite(trace)) {
@@ -434,6 +434,8 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     cs = warp_sum2(cs);
                     if (!(cabs2(cs) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
                     float a = atan2f(cs.y, cs.x);
+                    if (omx != nullptr) wx = -atan2f(zx.y, zx.x);   // Eq.(15)
+                    if (omy != nullptr) wy = atan2f(zy.y, zy.x);
                     if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
                     if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
                     if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
@@ -443,6 +445,8 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     const size_t o = (size_t)f * plane + (size_t)py * W + px;
                     out[o] = result;
                     if (flags != nullptr) flags[o] = fl;
+                    if (omx != nullptr) omx[o] = wx;
+                    if (omy != nullptr) omy[o] = wy;
                     if (COUNT) {
                         atomicAdd(counters + 0, 1ull);
                         atomicAdd(counters + 1, (unsigned long long)n_pow);

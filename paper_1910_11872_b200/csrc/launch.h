@@ -7,5 +7,6 @@
 namespace bos {
 template <int M, bool COUNT>
 cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
-                         uint8_t* flags, unsigned long long* counters, cudaStream_t s);
+                         uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
+                         cudaStream_t s);
 }  // namespace bos

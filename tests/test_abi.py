@@ -100,3 +100,13 @@ def test_product_path_does_not_import_oracle():
                 with open(os.path.join(dirpath, fn), encoding="utf-8") as fh:
                     src = fh.read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", src, re.M), fn
+
+
+def test_index_gradient_argument_errors(L):
+    g = L.bos_index_gradient
+    assert g(None, 10, 1.333, 1.0, 1e4, 0.01, None, None) == bosrm.BOS_ERR_INVALID_ARG
+    buf = ctypes.create_string_buffer(64)
+    p = ctypes.addressof(buf)
+    assert g(p, 0, 1.333, 1.0, 1e4, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG
+    assert g(p, 4, 1.333, 0.0, 1e4, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG
+    assert g(p, 4, 1.333, 1.0, -1.0, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG

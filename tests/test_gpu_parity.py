@@ -280,3 +280,37 @@ def test_c4_large_windows_sampled_parity(M):
     host = frames.cpu().numpy()
     o, ofl = R.demod_frame(host[1], M, pixels=(py, px))
     assert_parity(raw[1].cpu().numpy()[py, px], o, ofl, f"C4 M={M}")
+
+
+@pytest.mark.parametrize("M", [8, 11, 20])
+def test_omega_maps_match_oracle(M):
+    """Row f3: the Eq.(15) local frequencies ω_x = −arg z_x, ω_y = arg z_y (rad/pixel)."""
+    w = synth.workload("C2")
+    f = synth.make_frame(w, 1, snr_db=10.0)
+    out, fl, wx, wy = bosrm.bos_rootmusic_demod_ex(f.to(DEV), M, flags=True)
+    base, _ = bosrm.bos_rootmusic_demod(f.to(DEV), M)
+    torch.cuda.synchronize()
+    assert torch.equal(out, base)                      # the extra outputs do not change the phase
+    rng = np.random.default_rng(M)
+    pix = (rng.integers(0, w.H, 4096), rng.integers(0, w.W, 4096))
+    win, _ = R.extract_windows(f.numpy(), pix[0], pix[1], M)
+    res = R.estimate_windows(win)
+    assert_parity(wx[0].cpu().numpy()[pix], res["omega_x"], res["flags"], f"omega_x M={M}")
+    assert_parity(wy[0].cpu().numpy()[pix], res["omega_y"], res["flags"], f"omega_y M={M}")
+
+
+def test_index_gradient_kernel():
+    """Eq.(17) kernel vs the oracle formula, aligned and unaligned lengths, in place."""
+    for n in (1, 7, 4096, 1000003):
+        ph = torch.randn(n + 1, dtype=torch.float32, device=DEV)
+        for view in (ph[:n], ph[1:]):
+            v = view.contiguous() if view.storage_offset() == 0 else view
+            out = bosrm.bos_index_gradient(v, 1.333, 1.0, 1e4, 0.01)
+            torch.cuda.synchronize()
+            expect = R.index_gradient(v.cpu().numpy(), 1.333, 1.0, 1e4, 0.01)
+            assert np.allclose(out.cpu().numpy(), expect, rtol=1e-6, atol=0)
+    x = torch.randn(1000, dtype=torch.float32, device=DEV)
+    ref = x.clone()
+    bosrm.bos_index_gradient(x, 1.333, 1.0, 1e4, 0.01, out=x)   # in place
+    torch.cuda.synchronize()
+    assert np.allclose(x.cpu().numpy(), R.index_gradient(ref.cpu().numpy(), 1.333, 1.0, 1e4, 0.01), rtol=1e-6)

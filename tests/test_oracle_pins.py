@@ -399,3 +399,14 @@ def test_paper_tables_golden_parse():
     assert t1[np.argmin(t1[:, 2]), 0] == 4          # P:L323 minimum at L=4
     t2 = np.loadtxt(os.path.join(GOLDEN, "paper_table2_timing.txt"))
     assert np.allclose(t2[:, 1] / t2[:, 2], [29.5, 33.8, 35.1, 35.3], atol=0.1)
+
+
+def test_eq17_index_gradient_example():
+    """Eq.(17) with the SPEC example geometry: φ = 1 rad, μ = 1, f_x = 1e4 /m,
+    n0 = 1.333, L = 10 mm (the cell path length) → 0.6665 /m; linear in φ and n0,
+    inverse in μ and f_x, inverse-square in L."""
+    assert abs(R.index_gradient(1.0, 1.333, 1.0, 1e4, 0.01) - 0.6665) < 1e-12
+    base = R.index_gradient(2.0, 1.333, 1.0, 1e4, 0.01)
+    assert abs(base - 2 * 0.6665) < 1e-12
+    assert abs(R.index_gradient(1.0, 1.333, 2.0, 1e4, 0.01) - 0.6665 / 2) < 1e-12
+    assert abs(R.index_gradient(1.0, 1.333, 1.0, 1e4, 0.02) - 0.6665 / 4) < 1e-12
