@@ -159,6 +159,28 @@ int bos_index_gradient(const float* phase, size_t n, double n0, double mu, doubl
                        double cell_len, float* out, void* stream);
 
 /*
+ * bos_analytic_signal — SURVEY §8 row f1, the step before the path: the analytic (complex)
+ * fringe signal Γ of Eq.(1) from 8-bit intensity frames by "bandpass filtering and carrier
+ * removal".  Per frame: I/255 → 2-D FFT → keep the disc of radius `radius`
+ * (cycles/pixel) around the carrier (fx, fy) → inverse FFT → if `remove_carrier`,
+ * Γ·e^{−j2π(fx·x + fy·y)}.  The filter is a hard circular mask ([R11]; the paper names none).
+ *   frames_u8   DEVICE [n_frames][H][W] uint8 intensities.  H, W ≥ 2.
+ *   fx, fy      carrier in cycles/pixel, |fx|, |fy| ≤ 0.5; the disc must exclude DC
+ *               (fx² + fy² > radius²), else BOS_ERR_INVALID_ARG.
+ *   out         DEVICE [n_frames][H][W] bos_cf32, written (also the FFT buffer, in place);
+ *               must not overlap frames_u8.
+ *   d_workspace DEVICE cuFFT work area of ≥ bos_analytic_signal_workspace_bytes(H, W,
+ *               n_frames) bytes, caller-owned.
+ *   stream      cudaStream_t.  The FFTs use cuFFT (library FFT, plans made and destroyed per
+ *               call); the call returns after the work has completed (it synchronises
+ *               `stream` before destroying its plans).
+ */
+size_t bos_analytic_signal_workspace_bytes(int H, int W, int n_frames);
+int bos_analytic_signal(const uint8_t* frames_u8, int n_frames, int H, int W,
+                        double fx, double fy, double radius, int remove_carrier,
+                        bos_cf32* out, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
  * bos_rootmusic_iteration_counts — measurement support for the roofline:
  * runs the same kernel with per-pixel iteration counters over `frames` (DEVICE, as in
  * bos_rootmusic_demod) and accumulates into d_counters (DEVICE, 4 × uint64, caller zeroes):

@@ -27,3 +27,4 @@ from .rootmusic import (  # noqa: F401
     window_offsets,
     wrap,
 )
+from .analytic import analytic_signal, lobe_mask  # noqa: E402,F401

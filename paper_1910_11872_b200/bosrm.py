@@ -41,6 +41,9 @@ SIGNATURES = {
     "bos_rootmusic_demod_stack_host": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _SZ, _I, _VP]),
     "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
     "bos_rootmusic_demod_ex": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "bos_analytic_signal_workspace_bytes": (_SZ, [_I, _I, _I]),
+    "bos_analytic_signal": (_I, [_VP, _I, _I, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double, _I, _VP, _VP,
+                                 _SZ, _VP]),
     "bos_index_gradient": (_I, [_VP, _SZ, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                 _VP, _VP]),
     "bos_strerror": (ctypes.c_char_p, [_I]),
@@ -244,4 +247,24 @@ def bos_index_gradient(phase: torch.Tensor, n0: float, mu: float, f_x: float, ce
     rc = lib().bos_index_gradient(phase.data_ptr(), phase.numel(), float(n0), float(mu), float(f_x),
                                   float(cell_len), out.data_ptr(), _stream_ptr(stream))
     _check(rc, "bos_index_gradient")
+    return out
+
+
+def bos_analytic_signal(frames_u8: torch.Tensor, fx: float, fy: float, radius: float, remove_carrier: bool = False,
+                        out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """Row f1: uint8 CUDA frames [T,H,W] (or [H,W]) → analytic signal Γ complex64 [T,H,W]."""
+    frames_u8 = _dev_tensor(_frames3(frames_u8), torch.uint8, "frames_u8")
+    T, H, W = frames_u8.shape
+    if out is None:
+        out = torch.empty(T, H, W, dtype=torch.complex64, device=frames_u8.device)
+    _dev_tensor(out, torch.complex64, "out")
+    need = int(lib().bos_analytic_signal_workspace_bytes(H, W, T))
+    if workspace is None:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=frames_u8.device)
+    _dev_tensor(workspace, torch.uint8, "workspace")
+    rc = lib().bos_analytic_signal(frames_u8.data_ptr(), T, H, W, float(fx), float(fy), float(radius),
+                                   int(bool(remove_carrier)), out.data_ptr(), workspace.data_ptr(),
+                                   workspace.numel(), _stream_ptr(stream))
+    _check(rc, "bos_analytic_signal")
     return out

@@ -78,6 +78,9 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
     tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, "bos_rootmusic.cu"), "-o", host_obj],
                   host_obj + ".log"))
     objs = [host_obj]
+    an_obj = os.path.join(BUILD, "analytic.o")
+    tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, "analytic.cu"), "-o", an_obj], an_obj + ".log"))
+    objs.append(an_obj)
     for M in WINDOW_LENS:
         o = os.path.join(BUILD, f"demod_m{M}.o")
         objs.append(o)
@@ -93,7 +96,9 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
                 if "registers" in ln or "spill" in ln or "Compiling entry" in ln:
                     print(ln)
     tmp = LIB + ".tmp"
-    _run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs], os.path.join(BUILD, "link.log"))
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(cc)), "lib64")
+    _run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-L" + cudalib, "-lcufft",
+          "-Xlinker", "-rpath=" + cudalib], os.path.join(BUILD, "link.log"))
     os.replace(tmp, LIB)
     with open(stamp, "w") as fh:
         fh.write(digest)

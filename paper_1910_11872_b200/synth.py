@@ -170,3 +170,18 @@ def make_stack(w: Workload, frames=None, device="cpu", snr_db="default", out=Non
 def true_phase(w: Workload, t: int, device="cpu") -> torch.Tensor:
     """Analytic phase of frame t including the carrier (float64 [H,W], unwrapped)."""
     return carrier_phase(w.H, w.W, device) + w.phase(t, device)
+
+
+def make_intensity_frame(w: Workload, t: int, device="cpu", snr_db="default", visibility: float = 0.45,
+                         background: float = 0.5) -> torch.Tensor:
+    """8-bit carrier fringe intensity of frame t (the camera-side input of row f1):
+    I = 255·clip(b + v·cos(ω_c·r + φ_t) + n), n real Gaussian with E n² = v²/(2·10^{SNR/10}) (the
+    SNR of the analytic signal the bandpass recovers, amplitude v/2), quantised to uint8."""
+    snr = w.snr_db if snr_db == "default" else snr_db
+    ph = carrier_phase(w.H, w.W, device) + w.phase(t, device)
+    i = background + visibility * torch.cos(ph)
+    if snr is not None:
+        g = noise_generator(w.seed + 7919, t, device)
+        sigma = visibility * math.sqrt(0.5 / (10.0 ** (snr / 10.0)))
+        i = i + sigma * torch.randn(w.H, w.W, generator=g, device=device, dtype=torch.float64)
+    return torch.clamp(torch.round(i * 255.0), 0, 255).to(torch.uint8)

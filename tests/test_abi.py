@@ -110,3 +110,15 @@ def test_index_gradient_argument_errors(L):
     assert g(p, 0, 1.333, 1.0, 1e4, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG
     assert g(p, 4, 1.333, 0.0, 1e4, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG
     assert g(p, 4, 1.333, 1.0, -1.0, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG
+
+
+def test_analytic_signal_argument_errors(L):
+    f = L.bos_analytic_signal
+    buf = ctypes.create_string_buffer(4096)
+    p = ctypes.addressof(buf)
+    assert f(None, 1, 16, 16, 0.125, 0.0, 0.05, 0, p, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
+    # the disc around the carrier must exclude DC
+    assert f(p, 1, 16, 16, 0.03, 0.0, 0.05, 0, p + 1024, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
+    # carrier beyond Nyquist, non-positive radius
+    assert f(p, 1, 16, 16, 0.7, 0.0, 0.05, 0, p + 1024, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
+    assert f(p, 1, 16, 16, 0.2, 0.0, 0.0, 0, p + 1024, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
