@@ -1,0 +1,66 @@
+"""Row f1 measurement: analytic-signal front end (8-bit frames → Γ) and the camera-to-phase
+pipeline (f1 + root-MUSIC stack demod), 1024² × T frames on one B200.  CUDA events, warm-up,
+inputs resident in HBM.  Prints one JSON line.
+
+    python tools/bench_frontend.py --frames 100 --reps 5
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1910_11872_b200 import bosrm, synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--frames", type=int, default=100)
+    ap.add_argument("--size", type=int, default=1024)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--window-len", type=int, default=8)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    w = synth.workload("C3", H=args.size, W=args.size)
+    T = args.frames
+    u8 = torch.stack([synth.make_intensity_frame(w, t, device=dev) for t in range(T)])
+    gamma = torch.empty(T, w.H, w.W, dtype=torch.complex64, device=dev)
+    ws = torch.empty(max(256, int(bosrm.lib().bos_analytic_signal_workspace_bytes(w.H, w.W, T))),
+                     dtype=torch.uint8, device=dev)
+    out = torch.empty(T, w.H, w.W, dtype=torch.float32, device=dev)
+    ref = torch.empty(w.H, w.W, dtype=torch.float32, device=dev)
+
+    def f1():
+        bosrm.bos_analytic_signal(u8, synth.CARRIER_FX, synth.CARRIER_FY, 0.05, False, out=gamma, workspace=ws)
+
+    def pipe():
+        f1()
+        bosrm.bos_rootmusic_demod_stack(gamma, args.window_len, ref_index=0, ref_phase_out=ref, out_phase=out)
+
+    res = {}
+    for name, fn in (("analytic_signal", f1), ("pipeline_f1_plus_demod", pipe)):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.reps
+        mpx = T * w.H * w.W / (ms / 1e3) / 1e6
+        res[name] = {"ms": ms, "mpix_s": mpx, "frames_s": mpx / (w.H * w.W / 1e6)}
+    plane = w.H * w.W
+    # f1 DRAM traffic lower bound: 1 B in + 8 B out + 2 in-place FFTs (≥16 B r+w each) + mask (16 B) per pixel
+    bytes_px = 1 + 8 + 2 * 16 + 16
+    res["analytic_signal"]["achieved_gbs_lower_bound"] = bytes_px * T * plane / (res["analytic_signal"]["ms"] / 1e3) / 1e9
+    print(json.dumps({"workload": f"{w.H}x{w.W} x {T} 8-bit C3 intensity frames, carrier (1/16, 1/8), r = 0.05",
+                      "window_len": args.window_len, **res}))
+
+
+if __name__ == "__main__":
+    main()
