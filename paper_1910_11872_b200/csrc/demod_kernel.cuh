@@ -40,7 +40,7 @@ constexpr int kPolishMin = 2;         // Newton steps on the selected root after
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;
 constexpr float kRefineMargin = 0.05f; // selection margin (|ln|z||) below which the runner-up is polished too
-constexpr float kMoved2 = 1e-4f;       // polish displacement² that triggers tight re-convergence
+constexpr float kMoved2 = 1e-2f;       // polish displacement² (> 0.1) that triggers tight re-convergence
 constexpr float kAberthTightTol2 = 1e-10f;
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
@@ -480,10 +480,13 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             if (w2 < 1e30f) zs = csub(zs, w);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
                         }
-                        // A selected approximation that the polish moves far was not near a root
-                        // (loose sweeps can park an approximation between roots): converge all
-                        // roots tightly and select again.
-                        if (attempt == 0 && !(cabs2(csub(zs, zsel)) <= kMoved2)) {
+                        // Loose sweeps can park an approximation between roots; polished, it lands on
+                        // a root that is no longer the closest (or moves far).  Then converge all
+                        // roots tightly and select again.  (Near-double roots legitimately move
+                        // ~0.02 toward the circle during the polish: that is not a fallback.)
+                        const float dsel = ln_dist(zs), dsec = ln_dist(z2) - 1e-3f;
+                        if (attempt == 0 && (!(dsel <= dsec || marg == CUDART_INF_F) ||
+                                             !(cabs2(csub(zs, zsel)) <= kMoved2))) {
                             tol2 = kAberthTightTol2;
                             continue;
                         }

@@ -381,7 +381,9 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             if (w2 < 1e30f) zb = csub(zb, wp);
                             if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
                         }
-                        if (attempt == 0 && !(cabs2(csub(zb, zsel)) <= kMoved2)) {
+                        const float dsel = ln_dist(zb), dsec = ln_dist(z2) - 1e-3f;   // see demod_kernel.cuh
+                        if (attempt == 0 && (!(dsel <= dsec || !(second < CUDART_INF_F)) ||
+                                             !(cabs2(csub(zb, zsel)) <= kMoved2))) {
                             tol2 = kAberthTightTol2;
                             continue;
                         }
