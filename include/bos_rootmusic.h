@@ -181,6 +181,26 @@ int bos_analytic_signal(const uint8_t* frames_u8, int n_frames, int H, int W,
                         bos_cf32* out, void* d_workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * bos_unwrap — SURVEY §8 row f2, the step after the path: 2-D phase unwrapping "followed by
+ * an unwrapping operation" with the cited reliability-sorting algorithm (Herráez):
+ * reliability R = 1/sqrt(H²+V²+D1²+D2²) of wrapped second differences (edge-replicated
+ * neighbours), edges ranked by R(p)+R(q) (ties: edge id 2p horizontal / 2p+1 vertical),
+ * groups merged along the maximum spanning tree, one global 2π multiple fixed by the most
+ * reliable pixel ([R12]).  Built as Borůvka rounds + weighted union-find on the GPU; the
+ * 2π multiples equal the sequential FP64 algorithm's exactly (FP64 reliabilities).
+ *   wrapped     DEVICE [n_frames][H][W] float32 wrapped phase (e.g. out_phase of the demod).
+ *   unwrapped   DEVICE [n_frames][H][W] float32 = wrapped + 2π·k; may equal `wrapped`
+ *               (in place), must not partially overlap it.  NaN/Inf pixels stay as they are
+ *               (and count as 0 in the neighbours' second differences).
+ *   d_workspace DEVICE ≥ bos_unwrap_workspace_bytes(H, W) bytes, caller-owned; H·W < 2^31.
+ *   stream      cudaStream_t; the call is synchronous (it reads back a convergence flag
+ *               after each union round) and returns after the frames are done.
+ */
+size_t bos_unwrap_workspace_bytes(int H, int W);
+int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrapped,
+               void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
  * bos_rootmusic_iteration_counts — measurement support for the roofline:
  * runs the same kernel with per-pixel iteration counters over `frames` (DEVICE, as in
  * bos_rootmusic_demod) and accumulates into d_counters (DEVICE, 4 × uint64, caller zeroes):

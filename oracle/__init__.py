@@ -28,3 +28,4 @@ from .rootmusic import (  # noqa: F401
     wrap,
 )
 from .analytic import analytic_signal, lobe_mask  # noqa: E402,F401
+from . import unwrap  # noqa: E402,F401

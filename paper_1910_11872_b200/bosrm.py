@@ -42,6 +42,8 @@ SIGNATURES = {
     "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
     "bos_rootmusic_demod_ex": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     "bos_analytic_signal_workspace_bytes": (_SZ, [_I, _I, _I]),
+    "bos_unwrap_workspace_bytes": (_SZ, [_I, _I]),
+    "bos_unwrap": (_I, [_VP, _I, _I, _I, _VP, _VP, _SZ, _VP]),
     "bos_analytic_signal": (_I, [_VP, _I, _I, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double, _I, _VP, _VP,
                                  _SZ, _VP]),
     "bos_index_gradient": (_I, [_VP, _SZ, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
@@ -268,3 +270,21 @@ def bos_analytic_signal(frames_u8: torch.Tensor, fx: float, fy: float, radius: f
                                    workspace.numel(), _stream_ptr(stream))
     _check(rc, "bos_analytic_signal")
     return out
+
+
+def bos_unwrap(wrapped: torch.Tensor, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """Row f2: Herráez reliability-sorted unwrapping of CUDA float32 [T,H,W] (or [H,W]) phase maps."""
+    w = _dev_tensor(_frames3(wrapped), torch.float32, "wrapped")
+    T, H, W = w.shape
+    if out is None:
+        out = torch.empty_like(w)
+    _dev_tensor(out, torch.float32, "out")
+    need = int(lib().bos_unwrap_workspace_bytes(H, W))
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=w.device)
+    _dev_tensor(workspace, torch.uint8, "workspace")
+    rc = lib().bos_unwrap(w.data_ptr(), T, H, W, out.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                          _stream_ptr(stream))
+    _check(rc, "bos_unwrap")
+    return out.view(wrapped.shape)

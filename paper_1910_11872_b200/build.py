@@ -78,9 +78,10 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
     tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, "bos_rootmusic.cu"), "-o", host_obj],
                   host_obj + ".log"))
     objs = [host_obj]
-    an_obj = os.path.join(BUILD, "analytic.o")
-    tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, "analytic.cu"), "-o", an_obj], an_obj + ".log"))
-    objs.append(an_obj)
+    for src in ("analytic.cu", "unwrap.cu"):
+        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", o], o + ".log"))
+        objs.append(o)
     for M in WINDOW_LENS:
         o = os.path.join(BUILD, f"demod_m{M}.o")
         objs.append(o)

@@ -122,3 +122,12 @@ def test_analytic_signal_argument_errors(L):
     # carrier beyond Nyquist, non-positive radius
     assert f(p, 1, 16, 16, 0.7, 0.0, 0.05, 0, p + 1024, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
     assert f(p, 1, 16, 16, 0.2, 0.0, 0.0, 0, p + 1024, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
+
+
+def test_unwrap_workspace_and_errors(L):
+    n = 100 * 64
+    al = lambda v: (v + 255) // 256 * 256  # noqa: E731
+    expect = al(8 * n) + 4 * al(4 * n) + al(8 * n) + al(4 * n) + al(16) + al(8) + al(4)
+    assert L.bos_unwrap_workspace_bytes(100, 64) == expect
+    assert L.bos_unwrap_workspace_bytes(0, 5) == 0
+    assert L.bos_unwrap(None, 1, 8, 8, None, None, 0, None) == bosrm.BOS_ERR_INVALID_ARG
