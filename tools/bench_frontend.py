@@ -1,5 +1,5 @@
-"""Row f1 measurement: analytic-signal front end (8-bit frames → Γ) and the camera-to-phase
-pipeline (f1 + root-MUSIC stack demod), 1024² × T frames on one B200.  CUDA events, warm-up,
+"""Rows f1/f2 measurement: analytic-signal front end (8-bit frames → Γ), the camera-to-phase
+pipeline (f1 + root-MUSIC stack demod), the unwrapping step and the whole chain, 1024² × T frames on one B200.  CUDA events, warm-up,
 inputs resident in HBM.  Prints one JSON line.
 
     python tools/bench_frontend.py --frames 100 --reps 5
@@ -41,8 +41,19 @@ def main():
         f1()
         bosrm.bos_rootmusic_demod_stack(gamma, args.window_len, ref_index=0, ref_phase_out=ref, out_phase=out)
 
+    unw = torch.empty_like(out)
+    uws = torch.empty(int(bosrm.lib().bos_unwrap_workspace_bytes(w.H, w.W)), dtype=torch.uint8, device=dev)
+
+    def unwrap():
+        bosrm.bos_unwrap(out, out=unw, workspace=uws)
+
+    def full():
+        pipe()
+        unwrap()
+
     res = {}
-    for name, fn in (("analytic_signal", f1), ("pipeline_f1_plus_demod", pipe)):
+    for name, fn in (("analytic_signal", f1), ("pipeline_f1_plus_demod", pipe), ("unwrap", unwrap),
+                     ("pipeline_f1_demod_unwrap", full)):
         fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
