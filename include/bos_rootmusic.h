@@ -192,11 +192,13 @@ int bos_analytic_signal(const uint8_t* frames_u8, int n_frames, int H, int W,
  *   unwrapped   DEVICE [n_frames][H][W] float32 = wrapped + 2π·k; may equal `wrapped`
  *               (in place), must not partially overlap it.  NaN/Inf pixels stay as they are
  *               (and count as 0 in the neighbours' second differences).
- *   d_workspace DEVICE ≥ bos_unwrap_workspace_bytes(H, W) bytes, caller-owned; H·W < 2^31.
+ *   d_workspace DEVICE scratch, caller-owned: bos_unwrap_workspace_bytes(H, W, F) bytes lets the
+ *               call unwrap F frames per batch (one union-find forest); any size ≥ the 1-frame
+ *               figure works (fewer frames per batch).  2·F·H·W < 2^32.
  *   stream      cudaStream_t; the call is synchronous (it reads back a convergence flag
  *               after each union round) and returns after the frames are done.
  */
-size_t bos_unwrap_workspace_bytes(int H, int W);
+size_t bos_unwrap_workspace_bytes(int H, int W, int n_frames);
 int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrapped,
                void* d_workspace, size_t workspace_bytes, void* stream);
 

@@ -42,7 +42,7 @@ SIGNATURES = {
     "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
     "bos_rootmusic_demod_ex": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     "bos_analytic_signal_workspace_bytes": (_SZ, [_I, _I, _I]),
-    "bos_unwrap_workspace_bytes": (_SZ, [_I, _I]),
+    "bos_unwrap_workspace_bytes": (_SZ, [_I, _I, _I]),
     "bos_unwrap": (_I, [_VP, _I, _I, _I, _VP, _VP, _SZ, _VP]),
     "bos_analytic_signal": (_I, [_VP, _I, _I, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double, _I, _VP, _VP,
                                  _SZ, _VP]),
@@ -280,7 +280,7 @@ def bos_unwrap(wrapped: torch.Tensor, out: torch.Tensor | None = None, workspace
     if out is None:
         out = torch.empty_like(w)
     _dev_tensor(out, torch.float32, "out")
-    need = int(lib().bos_unwrap_workspace_bytes(H, W))
+    need = int(lib().bos_unwrap_workspace_bytes(H, W, T)) or int(lib().bos_unwrap_workspace_bytes(H, W, 1))
     if workspace is None:
         workspace = torch.empty(need, dtype=torch.uint8, device=w.device)
     _dev_tensor(workspace, torch.uint8, "workspace")

@@ -32,13 +32,14 @@ __device__ __forceinline__ double gam(double d) {
     return __dsub_rn(d, __dmul_rn(two_pi, c));
 }
 
-__global__ void reliability_kernel(const float* __restrict__ w, int H, int W, double* __restrict__ rel) {
-    const size_t n = (size_t)H * W;
+__global__ void reliability_kernel(const float* __restrict__ w, int H, int W, int F, double* __restrict__ rel) {
+    const size_t plane = (size_t)H * W, n = plane * F;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int y = (int)(i / W), x = (int)(i % W);
+        const size_t f0 = (i / plane) * plane, loc = i - f0;
+        const int y = (int)(loc / W), x = (int)(loc % W);
         auto at = [&](int dy, int dx) {
             const int yy = min(max(y + dy, 0), H - 1), xx = min(max(x + dx, 0), W - 1);
-            return fin(w[(size_t)yy * W + xx]);
+            return fin(w[f0 + (size_t)yy * W + xx]);
         };
         const double c = at(0, 0);
         const double h = __dsub_rn(gam(__dsub_rn(at(0, -1), c)), gam(__dsub_rn(c, at(0, 1))));
@@ -65,10 +66,12 @@ __global__ void reset_best(size_t n, unsigned long long* best_rel, unsigned* bes
     }
 }
 
-// edge id e = 2p (p → p+1) or 2p+1 (p → p+W); returns false for the missing border edges
+// edge id e = 2p (p → p+1) or 2p+1 (p → p+W), p = frame·H·W + y·W + x (a batch of frames is one
+// forest of independent grids); returns false for the missing border edges
 __device__ __forceinline__ bool edge_ends(unsigned e, int H, int W, int& p, int& q) {
     p = (int)(e >> 1);
-    const int x = p % W, y = p / W;
+    const int loc = p % (H * W);
+    const int x = loc % W, y = loc / W;
     if (e & 1u) {
         if (y + 1 >= H) return false;
         q = p + W;
@@ -80,9 +83,9 @@ __device__ __forceinline__ bool edge_ends(unsigned e, int H, int W, int& p, int&
 }
 
 // pass 1: every component's largest incident cross-edge reliability (positive doubles order as u64)
-__global__ void edge_max(int H, int W, const double* __restrict__ rel, const int* __restrict__ parent,
+__global__ void edge_max(int H, int W, int F, const double* __restrict__ rel, const int* __restrict__ parent,
                          unsigned long long* best_rel) {
-    const size_t ne = 2 * (size_t)H * W;
+    const size_t ne = 2 * (size_t)H * W * F;
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x) {
         int p, q;
         if (!edge_ends((unsigned)e, H, W, p, q)) continue;
@@ -95,9 +98,9 @@ __global__ void edge_max(int H, int W, const double* __restrict__ rel, const int
 }
 
 // pass 2: among the edges at that reliability, the smallest id
-__global__ void edge_argmin(int H, int W, const double* __restrict__ rel, const int* __restrict__ parent,
+__global__ void edge_argmin(int H, int W, int F, const double* __restrict__ rel, const int* __restrict__ parent,
                             const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
-    const size_t ne = 2 * (size_t)H * W;
+    const size_t ne = 2 * (size_t)H * W * F;
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x) {
         int p, q;
         if (!edge_ends((unsigned)e, H, W, p, q)) continue;
@@ -116,10 +119,10 @@ __device__ __forceinline__ int edge_k(const float* __restrict__ w, int a, int b)
 }
 
 // roots hook onto the root across their best edge (reads parent/off, writes parent2/off2)
-__global__ void hook(int H, int W, const float* __restrict__ w, const int* __restrict__ parent,
+__global__ void hook(int H, int W, int F, const float* __restrict__ w, const int* __restrict__ parent,
                      const int* __restrict__ off, const unsigned* __restrict__ best_id, int* __restrict__ parent2,
                      int* __restrict__ off2, int* __restrict__ hooked) {
-    const size_t n = (size_t)H * W;
+    const size_t n = (size_t)H * W * F;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const int c = (int)i;
         int np = parent[c], no = off[c];
@@ -154,19 +157,23 @@ __global__ void jump(size_t n, const int* __restrict__ parent, const int* __rest
     }
 }
 
-__global__ void anchor_max(size_t n, const double* __restrict__ rel, unsigned long long* best) {
+__global__ void anchor_max(size_t plane, int F, const double* __restrict__ rel, unsigned long long* best) {
+    const size_t n = plane * F;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        atomicMax(best, (unsigned long long)__double_as_longlong(rel[i]));
+        atomicMax(best + i / plane, (unsigned long long)__double_as_longlong(rel[i]));
 }
-__global__ void anchor_argmin(size_t n, const double* __restrict__ rel, const unsigned long long* best, unsigned* idx) {
+__global__ void anchor_argmin(size_t plane, int F, const double* __restrict__ rel, const unsigned long long* best,
+                              unsigned* idx) {
+    const size_t n = plane * F;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        if ((unsigned long long)__double_as_longlong(rel[i]) == *best) atomicMin(idx, (unsigned)i);
+        if ((unsigned long long)__double_as_longlong(rel[i]) == best[i / plane]) atomicMin(idx + i / plane, (unsigned)i);
 }
 
-__global__ void finish(size_t n, const float* __restrict__ w, const int* __restrict__ off, const unsigned* idx,
-                       float* __restrict__ out) {
-    const int k0 = off[*idx];
+__global__ void finish(size_t plane, int F, const float* __restrict__ w, const int* __restrict__ off,
+                       const unsigned* idx, float* __restrict__ out) {
+    const size_t n = plane * F;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int k0 = off[idx[i / plane]];
         const float v = w[i];
         out[i] = isfinite(v) ? (float)((double)v + 6.283185307179586 * (double)(off[i] - k0)) : v;
     }
@@ -184,7 +191,7 @@ struct Ws {
     unsigned* aidx;
 };
 
-size_t ws_layout(size_t n, char* base, Ws* ws) {
+size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
     size_t o = 0;
     auto take = [&](size_t bytes) {
         char* p = base ? base + o : nullptr;
@@ -199,8 +206,8 @@ size_t ws_layout(size_t n, char* base, Ws* ws) {
     char* br = take(n * sizeof(unsigned long long));
     char* bi = take(n * sizeof(unsigned));
     char* fl = take(4 * sizeof(int));
-    char* am = take(sizeof(unsigned long long));
-    char* ai = take(sizeof(unsigned));
+    char* am = take(F * sizeof(unsigned long long));
+    char* ai = take(F * sizeof(unsigned));
     if (ws) {
         ws->rel = (double*)r;
         ws->parent = (int*)p1;
@@ -229,59 +236,69 @@ bool is_dev(const void* p) {
 
 extern "C" {
 
-size_t bos_unwrap_workspace_bytes(int H, int W) {
-    if (H < 1 || W < 1 || (size_t)H * W * 2 >= 0xffffffffull) return 0;
-    return ws_layout((size_t)H * W, nullptr, nullptr);
+size_t bos_unwrap_workspace_bytes(int H, int W, int n_frames) {
+    if (H < 1 || W < 1 || n_frames < 1) return 0;
+    const size_t n = (size_t)H * W * n_frames;
+    if (n * 2 >= 0xffffffffull) return 0;
+    return ws_layout(n, n_frames, nullptr, nullptr);
 }
 
 int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrapped, void* d_workspace,
                size_t workspace_bytes, void* stream) {
     if (wrapped == nullptr || unwrapped == nullptr || d_workspace == nullptr || n_frames < 1 || H < 1 || W < 1)
         return BOS_ERR_INVALID_ARG;
-    const size_t n = (size_t)H * W;
-    if (n * 2 >= 0xffffffffull) return BOS_ERR_INVALID_ARG;          // edge ids are 32-bit
-    if (workspace_bytes < bos_unwrap_workspace_bytes(H, W)) return BOS_ERR_INVALID_ARG;
+    const size_t plane = (size_t)H * W;
+    if (plane * 2 >= 0xffffffffull) return BOS_ERR_INVALID_ARG;       // edge ids are 32-bit
+    // as many frames per batch as the workspace (and 32-bit ids) allow
+    int F = n_frames;
+    while (F > 1 && (bos_unwrap_workspace_bytes(H, W, F) == 0 || bos_unwrap_workspace_bytes(H, W, F) > workspace_bytes))
+        F = (F + 1) / 2;
+    if (workspace_bytes < bos_unwrap_workspace_bytes(H, W, F)) return BOS_ERR_INVALID_ARG;
     if (!is_dev(wrapped) || !is_dev(unwrapped) || !is_dev(d_workspace)) return BOS_ERR_INVALID_ARG;
     const uintptr_t a = (uintptr_t)wrapped, b = (uintptr_t)unwrapped;
-    const size_t tot = n * (size_t)n_frames * sizeof(float);
+    const size_t tot = plane * (size_t)n_frames * sizeof(float);
     if (a != b && a < b + tot && b < a + tot) return BOS_ERR_INVALID_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    Ws ws;
-    ws_layout(n, static_cast<char*>(d_workspace), &ws);
-    const unsigned gn = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
-    const unsigned ge = (unsigned)std::min<size_t>((2 * n + 255) / 256, 148 * 16);
     int host_flags[2];
-    for (int f = 0; f < n_frames; ++f) {
-        const float* w = wrapped + (size_t)f * n;
-        float* out = unwrapped + (size_t)f * n;
-        reliability_kernel<<<gn, 256, 0, s>>>(w, H, W, ws.rel);
+    for (int f0 = 0; f0 < n_frames; f0 += F) {
+        const int nf = std::min(F, n_frames - f0);
+        const size_t n = plane * nf;
+        Ws ws;
+        ws_layout(n, nf, static_cast<char*>(d_workspace), &ws);
+        const unsigned gn = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+        const unsigned ge = (unsigned)std::min<size_t>((2 * n + 255) / 256, 148 * 16);
+        const float* w = wrapped + (size_t)f0 * plane;
+        float* out = unwrapped + (size_t)f0 * plane;
+        reliability_kernel<<<gn, 256, 0, s>>>(w, H, W, nf, ws.rel);
         init_kernel<<<gn, 256, 0, s>>>(n, ws.parent, ws.off);
         for (int round = 0; round < 64; ++round) {                    // Borůvka: ≤ log2(n) rounds
             reset_best<<<gn, 256, 0, s>>>(n, ws.best_rel, ws.best_id);
-            edge_max<<<ge, 256, 0, s>>>(H, W, ws.rel, ws.parent, ws.best_rel);
-            edge_argmin<<<ge, 256, 0, s>>>(H, W, ws.rel, ws.parent, ws.best_rel, ws.best_id);
+            edge_max<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.parent, ws.best_rel);
+            edge_argmin<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.parent, ws.best_rel, ws.best_id);
             if (cudaMemsetAsync(ws.flags, 0, 2 * sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
-            hook<<<gn, 256, 0, s>>>(H, W, w, ws.parent, ws.off, ws.best_id, ws.parent2, ws.off2, ws.flags);
+            hook<<<gn, 256, 0, s>>>(H, W, nf, w, ws.parent, ws.off, ws.best_id, ws.parent2, ws.off2, ws.flags);
             std::swap(ws.parent, ws.parent2);
             std::swap(ws.off, ws.off2);
-            for (int j = 0; j < 64; ++j) {                                // compress to the roots
+            for (int j = 0; j < 64; j += 2) {                             // compress to the roots
                 if (cudaMemsetAsync(ws.flags + 1, 0, sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
-                jump<<<gn, 256, 0, s>>>(n, ws.parent, ws.off, ws.parent2, ws.off2, ws.flags + 1);
-                std::swap(ws.parent, ws.parent2);
-                std::swap(ws.off, ws.off2);
+                for (int t = 0; t < 2; ++t) {                             // two jumps per readback
+                    jump<<<gn, 256, 0, s>>>(n, ws.parent, ws.off, ws.parent2, ws.off2, ws.flags + 1);
+                    std::swap(ws.parent, ws.parent2);
+                    std::swap(ws.off, ws.off2);
+                }
                 if (cudaMemcpyAsync(host_flags, ws.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                     cudaStreamSynchronize(s) != cudaSuccess)
                     return BOS_ERR_CUDA;
                 if (!host_flags[1]) break;
             }
-            if (!host_flags[0]) break;                                  // nothing hooked: one tree left
+            if (!host_flags[0]) break;                                  // nothing hooked: one tree per frame
         }
-        if (cudaMemsetAsync(ws.amax, 0, sizeof(unsigned long long), s) != cudaSuccess ||
-            cudaMemsetAsync(ws.aidx, 0xff, sizeof(unsigned), s) != cudaSuccess)
+        if (cudaMemsetAsync(ws.amax, 0, nf * sizeof(unsigned long long), s) != cudaSuccess ||
+            cudaMemsetAsync(ws.aidx, 0xff, nf * sizeof(unsigned), s) != cudaSuccess)
             return BOS_ERR_CUDA;
-        anchor_max<<<gn, 256, 0, s>>>(n, ws.rel, ws.amax);
-        anchor_argmin<<<gn, 256, 0, s>>>(n, ws.rel, ws.amax, ws.aidx);
-        finish<<<gn, 256, 0, s>>>(n, w, ws.off, ws.aidx, out);
+        anchor_max<<<gn, 256, 0, s>>>(plane, nf, ws.rel, ws.amax);
+        anchor_argmin<<<gn, 256, 0, s>>>(plane, nf, ws.rel, ws.amax, ws.aidx);
+        finish<<<gn, 256, 0, s>>>(plane, nf, w, ws.off, ws.aidx, out);
         if (cudaGetLastError() != cudaSuccess) return BOS_ERR_CUDA;
     }
     return cudaStreamSynchronize(s) == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;

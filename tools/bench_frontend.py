@@ -42,7 +42,7 @@ def main():
         bosrm.bos_rootmusic_demod_stack(gamma, args.window_len, ref_index=0, ref_phase_out=ref, out_phase=out)
 
     unw = torch.empty_like(out)
-    uws = torch.empty(int(bosrm.lib().bos_unwrap_workspace_bytes(w.H, w.W)), dtype=torch.uint8, device=dev)
+    uws = torch.empty(int(bosrm.lib().bos_unwrap_workspace_bytes(w.H, w.W, T)), dtype=torch.uint8, device=dev)
 
     def unwrap():
         bosrm.bos_unwrap(out, out=unw, workspace=uws)
