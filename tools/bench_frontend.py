@@ -54,7 +54,8 @@ def main():
     res = {}
     for name, fn in (("analytic_signal", f1), ("pipeline_f1_plus_demod", pipe), ("unwrap", unwrap),
                      ("pipeline_f1_demod_unwrap", full)):
-        fn()
+        for _ in range(3):                  # warm-up (lazy module loading, cuFFT plan creation paths)
+            fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
