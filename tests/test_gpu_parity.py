@@ -314,3 +314,27 @@ def test_index_gradient_kernel():
     bosrm.bos_index_gradient(x, 1.333, 1.0, 1e4, 0.01, out=x)   # in place
     torch.cuda.synchronize()
     assert np.allclose(x.cpu().numpy(), R.index_gradient(ref.cpu().numpy(), 1.333, 1.0, 1e4, 0.01), rtol=1e-6)
+
+
+@pytest.mark.parametrize("M", [5, 8, 17, 24])
+def test_outputs_do_not_write_outside_their_buffers(M):
+    """Canary guard bands around out / flags / ω buffers (compute-sanitizer is not available on
+    this pool): every kernel writes exactly its [T,H,W] slice."""
+    T, H, W = 2, M + 5, 45
+    st = synth.make_stack(synth.workload("C3", H=H, W=W), frames=[0, 4], device=DEV)
+    n = T * H * W
+    pad = 4096
+    big = torch.full((n + 2 * pad,), 12345.0, dtype=torch.float32, device=DEV)
+    fbig = torch.full((n + 2 * pad,), 77, dtype=torch.uint8, device=DEV)
+    wx = torch.full((n + 2 * pad,), -7.0, dtype=torch.float32, device=DEV)
+    wy = torch.full((n + 2 * pad,), -8.0, dtype=torch.float32, device=DEV)
+    L = bosrm.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    rc = L.bos_rootmusic_demod_ex(st.data_ptr(), T, H, W, M, 3, None, big[pad:].data_ptr(), fbig[pad:].data_ptr(),
+                                  wx[pad:].data_ptr(), wy[pad:].data_ptr(), s)
+    assert rc == 0
+    torch.cuda.synchronize()
+    for buf, val in ((big, 12345.0), (wx, -7.0), (wy, -8.0)):
+        assert torch.all(buf[:pad] == val) and torch.all(buf[pad + n:] == val)
+        assert torch.all(torch.isfinite(buf[pad:pad + n]))
+    assert torch.all(fbig[:pad] == 77) and torch.all(fbig[pad + n:] == 77)
