@@ -59,31 +59,31 @@ def _run(cmd, log):
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False, defines=(), out: str | None = None) -> str:
     """Compile (if sources changed) and return the path of libbosrm.so.
     `defines` / `out` build a variant library (development A/B builds)."""
-    global BUILD, LIB
+    build_dir, lib = BUILD, LIB
     if out is not None:
-        BUILD = os.path.join(ROOT, "build", os.path.splitext(os.path.basename(out))[0])
-        LIB = out
-    os.makedirs(BUILD, exist_ok=True)
+        build_dir = os.path.join(ROOT, "build", os.path.splitext(os.path.basename(out))[0])
+        lib = out
+    os.makedirs(build_dir, exist_ok=True)
     extra = [f"-D{d}" for d in defines]
     digest = _sources_digest(extra)
-    stamp = os.path.join(BUILD, "stamp")
-    if not force and os.path.exists(LIB) and os.path.exists(stamp):
+    stamp = os.path.join(build_dir, "stamp")
+    if not force and os.path.exists(lib) and os.path.exists(stamp):
         with open(stamp) as fh:
             if fh.read().strip() == digest:
-                return LIB
+                return lib
     cc = nvcc()
     jobs = jobs or max(1, min(len(WINDOW_LENS) + 1, os.cpu_count() or 1))
     tasks = []
-    host_obj = os.path.join(BUILD, "bos_rootmusic.o")
+    host_obj = os.path.join(build_dir, "bos_rootmusic.o")
     tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, "bos_rootmusic.cu"), "-o", host_obj],
                   host_obj + ".log"))
     objs = [host_obj]
     for src in ("analytic.cu", "unwrap.cu"):
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         tasks.append(([cc, *NVFLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", o], o + ".log"))
         objs.append(o)
     for M in WINDOW_LENS:
-        o = os.path.join(BUILD, f"demod_m{M}.o")
+        o = os.path.join(build_dir, f"demod_m{M}.o")
         objs.append(o)
         tasks.append(([cc, *NVFLAGS, *extra, f"-DBOS_INST_M={M}", "-c", os.path.join(CSRC, "demod_inst.cu"), "-o", o],
                       o + ".log"))
@@ -96,14 +96,14 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
             for ln in out.splitlines():
                 if "registers" in ln or "spill" in ln or "Compiling entry" in ln:
                     print(ln)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cudalib = os.path.join(os.path.dirname(os.path.dirname(cc)), "lib64")
     _run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-L" + cudalib, "-lcufft",
-          "-Xlinker", "-rpath=" + cudalib], os.path.join(BUILD, "link.log"))
-    os.replace(tmp, LIB)
+          "-Xlinker", "-rpath=" + cudalib], os.path.join(build_dir, "link.log"))
+    os.replace(tmp, lib)
     with open(stamp, "w") as fh:
         fh.write(digest)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -26,7 +26,13 @@
 #include "cx2.cuh"
 #include "template_roots.h"
 
+#ifndef BOS_SWEEP_UNROLL
+#define BOS_SWEEP_UNROLL 1
+#endif
+
 namespace bos {
+
+constexpr int kSweepUnroll = BOS_SWEEP_UNROLL;   // root-update loop unroll factor (A/B builds)
 
 constexpr int kBX = 32;               // pixels per CTA along x (one warp per row)
 constexpr int kBY = 4;                // rows per CTA
@@ -42,6 +48,7 @@ constexpr float kPolishTol2 = 1e-12f;
 constexpr float kRefineMargin = 0.05f; // selection margin (|ln|z||) below which the runner-up is polished too
 constexpr float kMoved2 = 1e-2f;       // polish displacement² (> 0.1) that triggers tight re-convergence
 constexpr float kAberthTightTol2 = 1e-10f;
+
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
 constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
@@ -170,7 +177,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
     ok = false;
     for (; it < kAberthMaxIt; ++it) {
         float maxw = 0.0f;
-#pragma unroll 1
+#pragma unroll kSweepUnroll
         for (int r = 0; r < K; ++r) {
             const float2 zi = cx2_f2(z[0]);
             const float2 ratio = newton_ratio<N>(c, zi);
