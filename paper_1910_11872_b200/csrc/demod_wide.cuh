@@ -1,4 +1,4 @@
-// demod_wide.cuh — warp-per-pixel root-MUSIC demodulation for large windows (M = 17…32).
+// demod_wide.cuh — warp-per-pixel root-MUSIC demodulation for large windows (M = 19…32 by default).
 //
 // Same algorithm and arithmetic as demod_kernel.cuh (a1–a7, symmetric Aberth, Newton polish),
 // laid out for M where a thread can no longer hold R_y (M(M+1)/2 complex) in registers:
@@ -22,7 +22,10 @@
 
 namespace bos {
 
-constexpr int kWideMinM = 17;
+#ifndef BOS_WIDE_MIN_M
+#define BOS_WIDE_MIN_M 19
+#endif
+constexpr int kWideMinM = BOS_WIDE_MIN_M;   // smallest window handled warp-per-pixel
 
 __device__ __forceinline__ cx2 shfl_cx2(cx2 v, int src) {
     return (cx2)__shfl_sync(0xffffffffu, (unsigned long long)v, src);
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, wide_min_blocks<M>())
 demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                   const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
                   float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
-    static_assert(M >= kWideMinM && M <= 32, "wide kernel: 17 <= M <= 32");
+    static_assert(M >= 3 && M <= 32, "wide kernel: M <= 32");
     constexpr int N = 2 * M - 2;                 // polynomial degree
     constexpr int K = N / 2;                     // tracked (inside) roots, one per lane
     constexpr int O0 = (M - 1) / 2;              // o_i = i − O0  [R2]

@@ -94,7 +94,7 @@ def test_all_window_lengths_ragged_frame(M):
     warp-per-pixel kernel (M ≥ 17) wider than one 32-pixel segment, so the sliding R_y
     update runs)."""
     w = synth.workload("C2", H=37, W=45, seed=M)
-    H, W = (37, 45) if M < 17 else (M + 6, 75)
+    H, W = (37, 45) if M < 19 else (M + 6, 75)
     # smooth carrier fringe with mild phase, 10 dB
     f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M), 5, snr_db=10.0)
     g, gfl = run_gpu(f, M)
