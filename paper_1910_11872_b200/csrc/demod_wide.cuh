@@ -132,8 +132,11 @@ __device__ __forceinline__ float2 newton_ratio_warp(const cx2* __restrict__ c, f
     return cdiv(num, den);
 }
 
+#ifndef BOS_WIDE_BLOCKS
+#define BOS_WIDE_BLOCKS 0
+#endif
 template <int M>
-constexpr int wide_min_blocks() { return M <= 24 ? 3 : 2; }
+constexpr int wide_min_blocks() { return BOS_WIDE_BLOCKS > 0 ? BOS_WIDE_BLOCKS : (M <= 24 ? 3 : 2); }
 
 template <int M, bool COUNT>
 __global__ void __launch_bounds__(kThreads, wide_min_blocks<M>())
