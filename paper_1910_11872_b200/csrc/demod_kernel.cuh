@@ -50,6 +50,7 @@ constexpr float kMoved2 = 1e-2f;       // polish displacement² (> 0.1) that tri
 constexpr float kAberthTightTol2 = 1e-10f;
 
 constexpr float kNearCircle = 1e-2f;  // |1 − |z|²| below which z and 1/z̄ are one cluster
+constexpr float kReverse2 = 2.25f;    // |z|² beyond which P is evaluated through the reversed polynomial
 constexpr float kCos2TauOmega = 0.99990000333f; // cos²(1e-2): "distinct frequency" test
 constexpr float kTauSel = 1e-3f;      // AMBIGUOUS margin in |ln|z||
 constexpr float kLowAmp = 1e-4f;      // LOW_AMPLITUDE threshold
@@ -100,9 +101,10 @@ __device__ __forceinline__ constexpr int tri_off(int i, int j) {  // strict lowe
 // Q(u) = z^{−N}P(z) = conj(P(conj u)), u = 1/z:  P/P′ = z·Q/(N·Q − u·Q′), so Horner always
 // runs at |v| ≤ 1 (v = z or 1/z̄): no overflow for far roots, better relative accuracy.
 template <int N>
-__device__ __forceinline__ float2 newton_ratio(const cx2 (&c)[N + 1], float2 zi) {
+__device__ __forceinline__ void newton_num_den(const cx2 (&c)[N + 1], float2 zi, float2& num, float2& den) {
     const float m2 = cabs2(zi);
-    const bool outside = m2 > 1.0f;
+    // direct Horner up to |z| = 1.5 (|z|^N stays tame); beyond, the reversed polynomial
+    const bool outside = m2 > kReverse2;
     const float2 v = outside ? cscale(zi, __fdividef(1.0f, m2)) : zi;   // 1/z̄ or z
     // V and j·V as genuine 64-bit values (an f32x2 op result), so the register allocator keeps
     // each in one aligned pair instead of re-pairing scalars before every FFMA2.
@@ -115,12 +117,19 @@ __device__ __forceinline__ float2 newton_ratio(const cx2 (&c)[N + 1], float2 zi)
         dp = cmad2(dp, V, Vj, p);
         p = cmad2(p, V, Vj, c[k]);
     }
-    float2 num = cx2_f2(p), den = cx2_f2(dp);
+    num = cx2_f2(p);
+    den = cx2_f2(dp);
     if (outside) {
         const float2 q = cconj(num), dq = cconj(den), u = cconj(v);
         num = cmul(zi, q);
         den = csub(cscale(q, float(N)), cmul(u, dq));
     }
+}
+
+template <int N>
+__device__ __forceinline__ float2 newton_ratio(const cx2 (&c)[N + 1], float2 zi) {
+    float2 num, den;
+    newton_num_den<N>(c, zi, num, den);
     return cdiv(num, den);
 }
 
@@ -180,7 +189,8 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
 #pragma unroll kSweepUnroll
         for (int r = 0; r < K; ++r) {
             const float2 zi = cx2_f2(z[0]);
-            const float2 ratio = newton_ratio<N>(c, zi);
+            float2 num, den;                   // Newton ratio P/P′ = num/den
+            newton_num_den<N>(c, zi, num, den);
             // Own-mirror term.  Near the unit circle z and 1/z̄ merge into one (near-)double
             // root: keeping the term there freezes the tangential (arg = ω) error.  There the
             // update is Newton on P′ instead (a double root of P is a simple root of P′;
@@ -205,10 +215,8 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
                 sm = fma2(cx2_bcast(rcp_approx(q2)), d2, sm);
             }
             const float2 sf = cx2_f2(add2(s, sm));
-            // Aberth correction w = ratio / (1 − ratio·s)
-            const float2 d1 = make_float2(1.0f - (ratio.x * sf.x - ratio.y * sf.y),
-                                          -(ratio.x * sf.y + ratio.y * sf.x));
-            float2 w = cdiv(ratio, d1);
+            // Aberth correction w = (P/P′) / (1 − (P/P′)·s) = num / (den − num·s): one division
+            float2 w = cdiv(num, csub(den, cmul(num, sf)));
             if (near) w = newton_on_derivative<N>(c, zi);
             float w2 = cabs2(w);
             if (!(w2 < 1e30f)) {            // degenerate step (P′ = 0 or ratio·s = 1): skip
