@@ -332,11 +332,17 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
     for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
         const float2* __restrict__ frame = frames + (size_t)f * plane;
         // ---- a1: stage the clamped halo rows (Eq.(2) window support, [R1] clamp) ----
-        for (int idx = tx; idx < M * TW; idx += kBX) {
-            const int r = idx / TW, cc = idx - r * TW;
-            const int gy = min(max(py - O0 + r, 0), H - 1);
-            const int gx = min(max(x0 - O0 + cc, 0), W - 1);
-            tile[idx] = __ldg(frame + (size_t)gy * W + gx);
+        {
+            // row-wise: the clamped column offsets are per lane and frame-invariant, the row
+            // base is warp-uniform (no per-element division)
+            const int gx0 = min(max(x0 - O0 + tx, 0), W - 1);
+            const int gx1 = min(max(x0 - O0 + tx + kBX, 0), W - 1);
+#pragma unroll 2
+            for (int r = 0; r < M; ++r) {
+                const float2* __restrict__ row = frame + (size_t)min(max(py - O0 + r, 0), H - 1) * W;
+                tile[r * TW + tx] = __ldg(row + gx0);
+                if (tx + kBX < TW) tile[r * TW + tx + kBX] = __ldg(row + gx1);
+            }
         }
         __syncwarp();
 
