@@ -20,6 +20,9 @@ The oracle follows Algorithm 1 literally, for every pixel independe
   line 11 φ(px,py) ← Eq.(15)                                    estimate_windows  Eq.(15)
 
 plus the time-lapse reference difference wrap(φ_t − φ_ref) (BASELINE north_star, [R7]).
+Variant "fb" (NOT in the paper, [R13]): line 4 uses the eigenvectors of the
+forward–backward averaged covariances instead of the SVD (fb_subspaces); everything else is
+unchanged.
 Library primitives used as single steps: ``numpy.linalg.svd`` (LAPACK zgesdd) for the SVD
 and ``numpy.linalg.eigvals`` (LAPACK zgeev: balancing + Hessenberg + shifted QR) for the
 companion-matrix eigenvalues.  No blocking, fusion or reordering beyond the paper's steps.
@@ -100,6 +103,38 @@ def svd_subspaces(win: np.ndarray):
     is rank deficient (noise-free rank-1 windows)."""
     U, S, Vh = np.linalg.svd(win, full_matrices=True)
     return U, S, Vh
+
+
+def exchange(M: int) -> np.ndarray:
+    """J, the M×M exchange (anti-identity) matrix: (J x)_i = x_{M-1-i}."""
+    return np.eye(M)[::-1]
+
+
+def fb_average(R: np.ndarray) -> np.ndarray:
+    """Forward–backward average ½(R + J R* J) of covariances [N,M,M] (variant f4, NOT in the
+    paper): the covariance of the forward snapshots together with the backward snapshots
+    J·conj(x) (Pillai & Kwon 1989; standard in root-MUSIC/ESPRIT)."""
+    J = exchange(R.shape[-1])
+    return 0.5 * (R + J @ np.conj(R) @ J)
+
+
+def fb_subspaces(win: np.ndarray):
+    """Variant f4 replacement of Algorithm 1 line 4 (NOT in the paper): eigenvectors of the
+    forward–backward averaged R_y = Γ_wΓ_w^H and R_x = Γ_w^HΓ_w (Eq.(4) and its x-axis
+    counterpart), eigenvalues descending (numpy.linalg.eigh, LAPACK
+    zheevd, as a single step).  Returned like svd_subspaces: (U, S, V^H) with S = √λ(R_y,fb)."""
+    Wh = np.conj(np.swapaxes(win, 1, 2))
+    Ry = fb_average(win @ Wh)
+    Rx = fb_average(Wh @ win)
+    ly, U = np.linalg.eigh(Ry)
+    _, V = np.linalg.eigh(Rx)
+    U = U[:, :, ::-1]
+    V = V[:, :, ::-1]
+    S = np.sqrt(np.maximum(ly[:, ::-1], 0.0))
+    return U, S, np.conj(np.swapaxes(V, 1, 2))
+
+
+VARIANTS = ("paper", "fb")
 
 
 def noise_projectors(U: np.ndarray, Vh: np.ndarray):
@@ -205,13 +240,16 @@ def selection_margin(roots: np.ndarray, z_sel: np.ndarray) -> np.ndarray:
         return other.min(axis=1) - d_sel
 
 
-def estimate_windows(win: np.ndarray):
+def estimate_windows(win: np.ndarray, variant: str = "paper"):
     """Algorithm 1 lines 4-11 on a batch of windows [N,M,M] (complex128, finite).
+    variant "fb" (row f4, not in the paper) replaces line 4 by fb_subspaces.
 
     Returns dict: alpha (Eq.(15) phase), omega_x, omega_y, flags (bits 0-3), plus the
     intermediate z_y, z_x, S, margins for tests."""
     N, M, _ = win.shape
-    U, S, Vh = svd_subspaces(win)
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    U, S, Vh = svd_subspaces(win) if variant == "paper" else fb_subspaces(win)
     Cy, Cx = noise_projectors(U, Vh)
     ay = music_polynomial(Cy)
     ax = music_polynomial(Cx)
@@ -250,11 +288,11 @@ def default_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
-def _estimate_pixels(frame, py, px, M):
+def _estimate_pixels(frame, py, px, M, variant="paper"):
     win, border = extract_windows(frame, py, px, M)
     finite = np.isfinite(win.real).all(axis=(1, 2)) & np.isfinite(win.imag).all(axis=(1, 2))
     safe = np.where(finite[:, None, None], win, 0.0)
-    res = estimate_windows(safe)
+    res = estimate_windows(safe, variant)
     alpha = np.where(finite, res["alpha"], np.nan)
     flags = res["flags"].copy()
     flags[~finite] = FLAG_NONFINITE
@@ -263,7 +301,7 @@ def _estimate_pixels(frame, py, px, M):
 
 
 def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_phase=None,
-                pixels=None, threads: int | None = None, chunk: int | None = None):
+                pixels=None, threads: int | None = None, chunk: int | None = None, variant: str = "paper"):
     """Phase map of one frame: Algorithm 1 at every pixel (or at ``pixels=(py, px)``).
 
     ref_phase: None → raw α (wrapped); else out = wrap(α - ref_phase) [R7], where
@@ -294,7 +332,7 @@ def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_ph
 
     def work(j):
         s, e = bounds[j], bounds[j + 1]
-        alpha[s:e], flags[s:e] = _estimate_pixels(frame, py[s:e], px[s:e], M)
+        alpha[s:e], flags[s:e] = _estimate_pixels(frame, py[s:e], px[s:e], M, variant)
 
     if nthreads == 1 or len(bounds) <= 2:
         for j in range(len(bounds) - 1):
@@ -313,7 +351,7 @@ def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_ph
 
 
 def demod_stack(frames: np.ndarray, window_len: int, model_order: int = 3, ref_index: int = 0,
-                pixels=None, frame_indices=None, threads: int | None = None):
+                pixels=None, frame_indices=None, threads: int | None = None, variant: str = "paper"):
     """Time-lapse stack [T,H,W]: φ_ref = α(frames[ref_index]); out[t] = wrap(α_t - φ_ref).
 
     ``frame_indices`` restricts the output to those frames (sampled parity on big stacks);
@@ -322,10 +360,11 @@ def demod_stack(frames: np.ndarray, window_len: int, model_order: int = 3, ref_i
     frames = np.asarray(frames)
     T = frames.shape[0]
     ts = range(T) if frame_indices is None else frame_indices
-    ref, ref_flags = demod_frame(frames[ref_index], window_len, model_order, None, pixels, threads)
+    ref, ref_flags = demod_frame(frames[ref_index], window_len, model_order, None, pixels, threads,
+                                 variant=variant)
     outs, fls = [], []
     for t in ts:
-        a, f = demod_frame(frames[t], window_len, model_order, None, pixels, threads)
+        a, f = demod_frame(frames[t], window_len, model_order, None, pixels, threads, variant=variant)
         outs.append(wrap(a - ref))
         fls.append(f | ref_flags)
     return np.stack(outs), np.stack(fls)

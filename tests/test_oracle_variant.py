@@ -1,0 +1,142 @@
+"""Pins of the oracle's row-f4 variant (forward–backward averaged covariances, NOT in the
+paper; DESIGN.md [R13]).  CPU only.
+
+What pins it to something other than itself:
+* the textbook definition of FB averaging as the covariance of forward + backward snapshots
+  (the backward snapshot of x is J·conj(x)) — computed here by an SVD of the augmented data
+  matrix [Γ_w, J·conj(Γ_w)], a different route from fb_subspaces' eigh of ½(R + J R* J);
+* the Eq.(3) plane-wave model is still recovered exactly (odd and even M);
+* the backward window J·conj(Γ_w)·J has the same FB covariances, hence the same ω and the
+  conjugate phase;
+* the metamorphic invariants of the paper variant (transpose, global phase) still hold.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import rootmusic as R
+
+
+def noisy_windows(M, n, seed, sigma=0.7):
+    rng = np.random.default_rng(seed)
+    o = R.window_offsets(M)
+    wx = rng.uniform(-2, 2, n)
+    wy = rng.uniform(-2, 2, n)
+    a = rng.uniform(-math.pi, math.pi, n)
+    win = np.exp(1j * (wx[:, None, None] * o[None, None, :] + wy[:, None, None] * o[None, :, None]
+                       + a[:, None, None]))
+    return win + sigma * (rng.standard_normal(win.shape) + 1j * rng.standard_normal(win.shape))
+
+
+def test_exchange_matrix():
+    J = R.exchange(4)
+    assert np.array_equal(J @ np.arange(4), np.arange(4)[::-1])
+
+
+@pytest.mark.parametrize("M", [3, 6, 8, 11, 19, 32])
+def test_fb_equals_augmented_snapshot_svd(M):
+    """Dominant eigenvectors of the FB averages = dominant left singular vectors of the
+    augmented snapshot matrices [Γ, J Γ*] (y axis: columns are snapshots) and [Γ^T, J Γ^H]
+    conjugated (x axis: the rows of Γ read as snapshots of e^{-jω_x k} after conjugation,
+    v_1 ∝ Γ^H u_1 convention)."""
+    win = noisy_windows(M, 16, 300 + M)
+    J = R.exchange(M)
+    U, S, Vh = R.fb_subspaces(win)
+    for t in range(win.shape[0]):
+        G = win[t]
+        aug_y = np.concatenate([G, J @ np.conj(G)], axis=1)
+        uy = np.linalg.svd(aug_y)[0][:, 0]
+        # R_x = Γ^H Γ: its snapshots are the conjugated rows, conj(Γ)^T columns
+        Gx = np.conj(G).T
+        aug_x = np.concatenate([Gx, J @ np.conj(Gx)], axis=1)
+        ux = np.linalg.svd(aug_x)[0][:, 0]
+        v1 = np.conj(Vh[t, 0, :])          # first column of V
+        assert abs(abs(np.vdot(uy, U[t, :, 0])) - 1) < 1e-9
+        assert abs(abs(np.vdot(ux, v1)) - 1) < 1e-9
+        # eigenvalues: λ(R_fb) = σ²(aug)/2
+        s_aug = np.linalg.svd(aug_y, compute_uv=False)
+        assert np.allclose(S[t] ** 2, s_aug ** 2 / 2, rtol=1e-9, atol=1e-9 * s_aug[0] ** 2)
+
+
+def test_fb_average_is_centro_hermitian():
+    win = noisy_windows(7, 8, 5)
+    Rf = R.fb_average(win @ np.conj(np.swapaxes(win, 1, 2)))
+    J = R.exchange(7)
+    assert np.allclose(Rf, np.conj(np.swapaxes(Rf, 1, 2)), atol=1e-12)
+    assert np.allclose(Rf, J @ np.conj(Rf) @ J, atol=1e-12)
+
+
+@pytest.mark.parametrize("M", [3, 4, 5, 8, 11, 16, 17, 24, 32])
+def test_fb_plane_wave_exact(M):
+    rng = np.random.default_rng(400 + M)
+    n = 24
+    wx = rng.uniform(-2.5, 2.5, n)
+    wy = rng.uniform(-2.5, 2.5, n)
+    a = rng.uniform(-math.pi, math.pi, n)
+    o = R.window_offsets(M)
+    win = np.exp(1j * (wx[:, None, None] * o[None, None, :] + wy[:, None, None] * o[None, :, None]
+                       + a[:, None, None]))
+    r = R.estimate_windows(win, "fb")
+    assert np.max(np.abs(r["omega_x"] - wx)) < 1e-6
+    assert np.max(np.abs(r["omega_y"] - wy)) < 1e-6
+    tol = 1e-9 if M % 2 else 1e-6
+    assert np.max(np.abs(R.wrap(r["alpha"] - a))) < tol
+    assert not np.any(r["flags"] & R.PARITY_EXCLUDE_MASK)
+
+
+@pytest.mark.parametrize("M", [5, 8, 11])
+def test_fb_backward_window_symmetry(M):
+    """Γ' = J Γ* J has the same FB covariances ⇒ identical ω; α' = −α − (ω_x + ω_y)·δ with
+    δ = 0 (odd M, centred window) or 1 (even M: o_{M−1−i} = 1 − o_i, [R2])."""
+    win = noisy_windows(M, 64, 500 + M)
+    J = R.exchange(M)
+    back = J @ np.conj(win) @ J
+    f0, f1 = R.estimate_windows(win, "fb"), R.estimate_windows(back, "fb")
+    ok = ((f0["flags"] | f1["flags"]) & R.PARITY_EXCLUDE_MASK) == 0
+    assert ok.mean() > 0.8
+    delta = 0.0 if M % 2 else 1.0
+    assert np.max(np.abs(R.wrap(f1["omega_x"] - f0["omega_x"]))[ok]) < 1e-9
+    assert np.max(np.abs(R.wrap(f1["omega_y"] - f0["omega_y"]))[ok]) < 1e-9
+    pred = -f0["alpha"] - delta * (f0["omega_x"] + f0["omega_y"])
+    assert np.max(np.abs(R.wrap(f1["alpha"] - pred))[ok]) < 1e-9
+    # (root-MUSIC itself has this symmetry — the polynomial of J·conj(u) equals that of u —
+    # so the paper variant passes it too; for FB it pins the J·R*·J term: an FB average that
+    # drops the conjugate or one J breaks the equality of the two FB covariances)
+
+
+@pytest.mark.parametrize("M", [3, 8])
+def test_fb_metamorphic(M):
+    win = noisy_windows(M, 64, 600 + M)
+    base = R.estimate_windows(win, "fb")
+    ok = (base["flags"] & R.PARITY_EXCLUDE_MASK) == 0
+    tr = R.estimate_windows(np.swapaxes(win, 1, 2).copy(), "fb")
+    assert np.max(np.abs(R.wrap(tr["alpha"] - base["alpha"]))[ok]) < 1e-9
+    assert np.max(np.abs(R.wrap(tr["omega_x"] - base["omega_y"]))[ok]) < 1e-9
+    sh = R.estimate_windows(2.5 * np.exp(0.77j) * win, "fb")
+    assert np.max(np.abs(R.wrap(sh["alpha"] - base["alpha"] - 0.77))[ok]) < 1e-9
+
+
+def test_fb_differs_from_paper_on_noise_but_agrees_statistically():
+    """Both variants estimate the same plane: on 10 dB-like windows the two phase maps agree
+    to well within the noise (not bit-identical: different subspace estimates)."""
+    win = noisy_windows(11, 256, 700, sigma=0.2)
+    a = R.estimate_windows(win, "paper")
+    b = R.estimate_windows(win, "fb")
+    d = np.abs(R.wrap(a["alpha"] - b["alpha"]))
+    assert d.max() > 1e-8
+    assert np.median(d) < 0.02
+
+
+def test_unknown_variant_rejected():
+    with pytest.raises(ValueError):
+        R.estimate_windows(noisy_windows(3, 1, 0), "spatial")
+
+
+def test_demod_frame_variant_threading():
+    rng = np.random.default_rng(9)
+    f = (rng.standard_normal((20, 21)) + 1j * rng.standard_normal((20, 21))).astype(np.complex64)
+    a1, f1 = R.demod_frame(f, 5, variant="fb", threads=1)
+    a2, f2 = R.demod_frame(f, 5, variant="fb", threads=4)
+    assert np.array_equal(a1, a2) and np.array_equal(f1, f2)
