@@ -122,16 +122,18 @@ def fb_subspaces(win: np.ndarray):
     """Variant f4 replacement of Algorithm 1 line 4 (NOT in the paper): eigenvectors of the
     forward–backward averaged R_y = Γ_wΓ_w^H and R_x = Γ_w^HΓ_w (Eq.(4) and its x-axis
     counterpart), eigenvalues descending (numpy.linalg.eigh, LAPACK
-    zheevd, as a single step).  Returned like svd_subspaces: (U, S, V^H) with S = √λ(R_y,fb)."""
+    zheevd, as a single step).  Returned like svd_subspaces, (U, S, V^H) with S = √λ(R_y,fb),
+    plus S_x = √λ(R_x,fb): unlike the SVD, the two axes have different spectra."""
     Wh = np.conj(np.swapaxes(win, 1, 2))
     Ry = fb_average(win @ Wh)
     Rx = fb_average(Wh @ win)
     ly, U = np.linalg.eigh(Ry)
-    _, V = np.linalg.eigh(Rx)
+    lx, V = np.linalg.eigh(Rx)
     U = U[:, :, ::-1]
     V = V[:, :, ::-1]
     S = np.sqrt(np.maximum(ly[:, ::-1], 0.0))
-    return U, S, np.conj(np.swapaxes(V, 1, 2))
+    Sx = np.sqrt(np.maximum(lx[:, ::-1], 0.0))
+    return U, S, np.conj(np.swapaxes(V, 1, 2)), Sx
 
 
 VARIANTS = ("paper", "fb")
@@ -249,7 +251,11 @@ def estimate_windows(win: np.ndarray, variant: str = "paper"):
     N, M, _ = win.shape
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
-    U, S, Vh = svd_subspaces(win) if variant == "paper" else fb_subspaces(win)
+    if variant == "paper":
+        U, S, Vh = svd_subspaces(win)
+        Sx = S                       # one spectrum: σ of Γ_w serves both axes
+    else:
+        U, S, Vh, Sx = fb_subspaces(win)
     Cy, Cx = noise_projectors(U, Vh)
     ay = music_polynomial(Cy)
     ax = music_polynomial(Cx)
@@ -272,7 +278,9 @@ def estimate_windows(win: np.ndarray, variant: str = "paper"):
     marg = np.minimum(selection_margin(ry, zy), selection_margin(rx, zx))
     flags |= np.where(marg < TAU_SEL, FLAG_AMBIGUOUS, 0).astype(np.uint8)
     with np.errstate(divide="ignore", invalid="ignore"):
-        gap = np.where(S[:, 1] > 0, (S[:, 0] / S[:, 1]) ** 2, np.inf)
+        # [R8]/[R13]: the smaller eigenvalue ratio of the two axes' covariances
+        gap = np.minimum(np.where(S[:, 1] > 0, (S[:, 0] / S[:, 1]) ** 2, np.inf),
+                         np.where(Sx[:, 1] > 0, (Sx[:, 0] / Sx[:, 1]) ** 2, np.inf))
     flags |= np.where(gap < GAMMA_MIN, FLAG_SMALL_GAP, 0).astype(np.uint8)
     fro = np.sqrt(np.sum(np.abs(win) ** 2, axis=(1, 2)))
     low = (fro == 0) | (np.abs(c) * M * M < LOW_AMP * M * fro)

@@ -43,7 +43,7 @@ def test_fb_equals_augmented_snapshot_svd(M):
     v_1 ∝ Γ^H u_1 convention)."""
     win = noisy_windows(M, 16, 300 + M)
     J = R.exchange(M)
-    U, S, Vh = R.fb_subspaces(win)
+    U, S, Vh, Sx = R.fb_subspaces(win)
     for t in range(win.shape[0]):
         G = win[t]
         aug_y = np.concatenate([G, J @ np.conj(G)], axis=1)
@@ -58,6 +58,8 @@ def test_fb_equals_augmented_snapshot_svd(M):
         # eigenvalues: λ(R_fb) = σ²(aug)/2
         s_aug = np.linalg.svd(aug_y, compute_uv=False)
         assert np.allclose(S[t] ** 2, s_aug ** 2 / 2, rtol=1e-9, atol=1e-9 * s_aug[0] ** 2)
+        s_augx = np.linalg.svd(aug_x, compute_uv=False)
+        assert np.allclose(Sx[t] ** 2, s_augx ** 2 / 2, rtol=1e-9, atol=1e-9 * s_augx[0] ** 2)
 
 
 def test_fb_average_is_centro_hermitian():
@@ -127,6 +129,22 @@ def test_fb_differs_from_paper_on_noise_but_agrees_statistically():
     d = np.abs(R.wrap(a["alpha"] - b["alpha"]))
     assert d.max() > 1e-8
     assert np.median(d) < 0.02
+
+
+def test_fb_small_gap_uses_both_axes():
+    """[R13]: a window whose columns are clamped copies (frame border) has a well-separated
+    R_y but a near-degenerate FB R_x; SMALL_GAP must fire on the x axis alone."""
+    rng = np.random.default_rng(3)
+    M = 32
+    o = R.window_offsets(M)
+    win = np.exp(1j * (0.4 * o[None, :] + 0.7 * o[:, None]))
+    win = win + 0.05 * (rng.standard_normal(win.shape) + 1j * rng.standard_normal(win.shape))
+    win[:, M // 2:] = win[:, M // 2 - 1:M // 2]        # clamp at x = W−1 (M = 32 border pixel)
+    U, S, Vh, Sx = R.fb_subspaces(win[None])
+    gy, gx = (S[0, 0] / S[0, 1]) ** 2, (Sx[0, 0] / Sx[0, 1]) ** 2
+    assert gy > R.GAMMA_MIN > gx
+    assert R.estimate_windows(win[None], "fb")["flags"][0] & R.FLAG_SMALL_GAP
+    assert not R.estimate_windows(win[None], "paper")["flags"][0] & R.FLAG_SMALL_GAP
 
 
 def test_unknown_variant_rejected():
