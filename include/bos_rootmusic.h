@@ -66,6 +66,12 @@ enum {
 #define BOS_WINDOW_LEN_MAX 32
 #define BOS_MODEL_ORDER 3   /* Eq.(3): φ_w = α + ω_x x + ω_y y, three parameters [R3] */
 
+/* Covariance variants for bos_rootmusic_demod_variant. */
+enum {
+    BOS_VARIANT_PAPER = 0,  /* Algorithm 1 as published: singular vectors of Γ_w */
+    BOS_VARIANT_FB = 1      /* NOT in the paper: forward–backward averaged covariances, see below */
+};
+
 /*
  * bos_rootmusic_demod — demodulate n_frames frames (Algorithm 1 over every pixel).
  *
@@ -143,6 +149,23 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W,
                            int window_len, int model_order, const float* ref_phase,
                            float* out_phase, uint8_t* flags, float* omega_x, float* omega_y,
                            void* stream);
+
+/*
+ * bos_rootmusic_demod_variant — bos_rootmusic_demod_ex with a selectable covariance
+ * (a standard root-MUSIC extension the paper does NOT use; the paper's
+ * Algorithm 1 is variant BOS_VARIANT_PAPER, identical to bos_rootmusic_demod_ex).
+ *   variant  BOS_VARIANT_PAPER: u_1, v_1 = dominant singular vectors of Γ_w (Algorithm 1 l.4).
+ *            BOS_VARIANT_FB: u_1 = dominant eigenvector of ½(R_y + J R_y* J), R_y = Γ_wΓ_w^H,
+ *            v_1 = dominant eigenvector of ½(R_x + J R_x* J), R_x = Γ_w^HΓ_w (J: the M×M
+ *            exchange matrix; the backward snapshots J·conj(column)).  Both are exact for the
+ *            Eq.(3) plane-wave model; the rest of Algorithm 1 (Eqs.(12),(13), root selection,
+ *            Eq.(15)) is unchanged.  Any other value: BOS_ERR_UNSUPPORTED.
+ * Other arguments, errors and determinism as bos_rootmusic_demod_ex.
+ */
+int bos_rootmusic_demod_variant(const bos_cf32* frames, int n_frames, int H, int W,
+                                int window_len, int model_order, int variant,
+                                const float* ref_phase, float* out_phase, uint8_t* flags,
+                                float* omega_x, float* omega_y, void* stream);
 
 /*
  * bos_index_gradient — Eq.(17): the refractive-index derivative is

@@ -32,6 +32,9 @@ WINDOW_LEN_MIN = 3
 WINDOW_LEN_MAX = 32
 MODEL_ORDER = 3
 
+VARIANT_PAPER = 0   # Algorithm 1 as published
+VARIANT_FB = 1      # row f4: forward–backward averaged covariances (not in the paper)
+
 # name -> (restype, argtypes); must match include/bos_rootmusic.h
 _VP, _I, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
 SIGNATURES = {
@@ -41,6 +44,7 @@ SIGNATURES = {
     "bos_rootmusic_demod_stack_host": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _SZ, _I, _VP]),
     "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
     "bos_rootmusic_demod_ex": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "bos_rootmusic_demod_variant": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     "bos_analytic_signal_workspace_bytes": (_SZ, [_I, _I, _I]),
     "bos_unwrap_workspace_bytes": (_SZ, [_I, _I, _I]),
     "bos_unwrap": (_I, [_VP, _I, _I, _I, _VP, _VP, _SZ, _VP]),
@@ -70,6 +74,8 @@ def lib() -> ctypes.CDLL:
                                "`python -m paper_1910_11872_b200.build` (no CPU fallback exists)")
         L = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if "BOS_LIBRARY" in os.environ and not hasattr(L, name):
+                continue                      # A/B builds of older revisions may lack new entries
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
@@ -236,6 +242,30 @@ def bos_rootmusic_demod_ex(frames: torch.Tensor, window_len: int = 8, model_orde
         fl.data_ptr() if fl is not None else None, wx.data_ptr() if wx is not None else None,
         wy.data_ptr() if wy is not None else None, _stream_ptr(stream))
     _check(rc, "bos_rootmusic_demod_ex")
+    return out, fl, wx, wy
+
+
+def bos_rootmusic_demod_variant(frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
+                                variant: int = VARIANT_FB, ref_phase: torch.Tensor | None = None,
+                                out_phase: torch.Tensor | None = None, flags=None, omega=False, stream=None):
+    """bos_rootmusic_demod_ex with a covariance variant (VARIANT_PAPER / VARIANT_FB)
+    → (phase, flags|None, ω_x|None, ω_y|None)."""
+    frames = _dev_tensor(_frames3(frames), torch.complex64, "frames")
+    T, H, W = frames.shape
+    dev = frames.device
+    out = out_phase if out_phase is not None else torch.empty(T, H, W, dtype=torch.float32, device=dev)
+    _dev_tensor(out, torch.float32, "out_phase")
+    fl = torch.empty(T, H, W, dtype=torch.uint8, device=dev) if flags else None
+    wx = torch.empty(T, H, W, dtype=torch.float32, device=dev) if omega else None
+    wy = torch.empty(T, H, W, dtype=torch.float32, device=dev) if omega else None
+    if ref_phase is not None:
+        _dev_tensor(ref_phase, torch.float32, "ref_phase")
+    rc = lib().bos_rootmusic_demod_variant(
+        frames.data_ptr(), T, H, W, int(window_len), int(model_order), int(variant),
+        ref_phase.data_ptr() if ref_phase is not None else None, out.data_ptr(),
+        fl.data_ptr() if fl is not None else None, wx.data_ptr() if wx is not None else None,
+        wy.data_ptr() if wy is not None else None, _stream_ptr(stream))
+    _check(rc, "bos_rootmusic_demod_variant")
     return out, fl, wx, wy
 
 

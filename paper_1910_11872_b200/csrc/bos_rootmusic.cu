@@ -15,39 +15,39 @@ namespace {
 using LaunchFn = cudaError_t (*)(const float2*, int, int, int, const float*, float*, uint8_t*, float*, float*,
                                  unsigned long long*, cudaStream_t);
 
-template <bool COUNT>
+template <bool COUNT, bool FB>
 LaunchFn pick(int M) {
     switch (M) {
-        case 3: return bos::launch_demod<3, COUNT>;
-        case 4: return bos::launch_demod<4, COUNT>;
-        case 5: return bos::launch_demod<5, COUNT>;
-        case 6: return bos::launch_demod<6, COUNT>;
-        case 7: return bos::launch_demod<7, COUNT>;
-        case 8: return bos::launch_demod<8, COUNT>;
-        case 9: return bos::launch_demod<9, COUNT>;
-        case 10: return bos::launch_demod<10, COUNT>;
-        case 11: return bos::launch_demod<11, COUNT>;
-        case 12: return bos::launch_demod<12, COUNT>;
-        case 13: return bos::launch_demod<13, COUNT>;
-        case 14: return bos::launch_demod<14, COUNT>;
-        case 15: return bos::launch_demod<15, COUNT>;
-        case 16: return bos::launch_demod<16, COUNT>;
-        case 17: return bos::launch_demod<17, COUNT>;
-        case 18: return bos::launch_demod<18, COUNT>;
-        case 19: return bos::launch_demod<19, COUNT>;
-        case 20: return bos::launch_demod<20, COUNT>;
-        case 21: return bos::launch_demod<21, COUNT>;
-        case 22: return bos::launch_demod<22, COUNT>;
-        case 23: return bos::launch_demod<23, COUNT>;
-        case 24: return bos::launch_demod<24, COUNT>;
-        case 25: return bos::launch_demod<25, COUNT>;
-        case 26: return bos::launch_demod<26, COUNT>;
-        case 27: return bos::launch_demod<27, COUNT>;
-        case 28: return bos::launch_demod<28, COUNT>;
-        case 29: return bos::launch_demod<29, COUNT>;
-        case 30: return bos::launch_demod<30, COUNT>;
-        case 31: return bos::launch_demod<31, COUNT>;
-        case 32: return bos::launch_demod<32, COUNT>;
+        case 3: return bos::launch_demod<3, COUNT, FB>;
+        case 4: return bos::launch_demod<4, COUNT, FB>;
+        case 5: return bos::launch_demod<5, COUNT, FB>;
+        case 6: return bos::launch_demod<6, COUNT, FB>;
+        case 7: return bos::launch_demod<7, COUNT, FB>;
+        case 8: return bos::launch_demod<8, COUNT, FB>;
+        case 9: return bos::launch_demod<9, COUNT, FB>;
+        case 10: return bos::launch_demod<10, COUNT, FB>;
+        case 11: return bos::launch_demod<11, COUNT, FB>;
+        case 12: return bos::launch_demod<12, COUNT, FB>;
+        case 13: return bos::launch_demod<13, COUNT, FB>;
+        case 14: return bos::launch_demod<14, COUNT, FB>;
+        case 15: return bos::launch_demod<15, COUNT, FB>;
+        case 16: return bos::launch_demod<16, COUNT, FB>;
+        case 17: return bos::launch_demod<17, COUNT, FB>;
+        case 18: return bos::launch_demod<18, COUNT, FB>;
+        case 19: return bos::launch_demod<19, COUNT, FB>;
+        case 20: return bos::launch_demod<20, COUNT, FB>;
+        case 21: return bos::launch_demod<21, COUNT, FB>;
+        case 22: return bos::launch_demod<22, COUNT, FB>;
+        case 23: return bos::launch_demod<23, COUNT, FB>;
+        case 24: return bos::launch_demod<24, COUNT, FB>;
+        case 25: return bos::launch_demod<25, COUNT, FB>;
+        case 26: return bos::launch_demod<26, COUNT, FB>;
+        case 27: return bos::launch_demod<27, COUNT, FB>;
+        case 28: return bos::launch_demod<28, COUNT, FB>;
+        case 29: return bos::launch_demod<29, COUNT, FB>;
+        case 30: return bos::launch_demod<30, COUNT, FB>;
+        case 31: return bos::launch_demod<31, COUNT, FB>;
+        case 32: return bos::launch_demod<32, COUNT, FB>;
         default: return nullptr;
     }
 }
@@ -78,7 +78,8 @@ int check_common(int n_frames, int H, int W, int window_len, int model_order) {
 
 int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_len, int model_order,
                const float* ref_phase, float* out_phase, uint8_t* flags, unsigned long long* counters,
-               void* stream, bool check_ptrs, float* omega_x = nullptr, float* omega_y = nullptr) {
+               void* stream, bool check_ptrs, float* omega_x = nullptr, float* omega_y = nullptr,
+               int variant = BOS_VARIANT_PAPER) {
     int rc = check_common(n_frames, H, W, window_len, model_order);
     if (rc != BOS_OK) return rc;
     if (frames == nullptr || out_phase == nullptr) return BOS_ERR_INVALID_ARG;
@@ -103,7 +104,10 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
         if (ref_phase != nullptr && !is_device_ptr(ref_phase)) return BOS_ERR_INVALID_ARG;
         if (flags != nullptr && !is_device_ptr(flags)) return BOS_ERR_INVALID_ARG;
     }
-    LaunchFn fn = counters ? pick<true>(window_len) : pick<false>(window_len);
+    if (variant != BOS_VARIANT_PAPER && variant != BOS_VARIANT_FB) return BOS_ERR_UNSUPPORTED;
+    if (variant == BOS_VARIANT_FB && counters != nullptr) return BOS_ERR_UNSUPPORTED;
+    LaunchFn fn = variant == BOS_VARIANT_FB ? pick<false, true>(window_len)
+                                            : (counters ? pick<true, false>(window_len) : pick<false, false>(window_len));
     if (fn == nullptr) return BOS_ERR_UNSUPPORTED;
     const cudaError_t e = fn(reinterpret_cast<const float2*>(frames), n_frames, H, W, ref_phase, out_phase,
                              flags, omega_x, omega_y, counters, static_cast<cudaStream_t>(stream));
@@ -136,13 +140,13 @@ __global__ void index_gradient_kernel(const float* __restrict__ phase, size_t n,
 
 extern "C" {
 
-int bos_abi_version(void) { return (1 << 16) | 0; }
+int bos_abi_version(void) { return (1 << 16) | 1; }
 
 const char* bos_strerror(int code) {
     switch (code) {
         case BOS_OK: return "ok";
         case BOS_ERR_INVALID_ARG: return "invalid argument (NULL pointer, size, aliasing or host/device pointer)";
-        case BOS_ERR_UNSUPPORTED: return "unsupported (model_order must be 3; window_len outside the instantiated range)";
+        case BOS_ERR_UNSUPPORTED: return "unsupported (model_order must be 3; window_len outside the instantiated range; unknown variant)";
         case BOS_ERR_CUDA: return "CUDA runtime error or kernel launch failure";
         default: return "unknown bos_rootmusic status code";
     }
@@ -159,6 +163,13 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W, i
                            void* stream) {
     return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, flags, nullptr,
                       stream, true, omega_x, omega_y);
+}
+
+int bos_rootmusic_demod_variant(const bos_cf32* frames, int n_frames, int H, int W, int window_len,
+                                int model_order, int variant, const float* ref_phase, float* out_phase,
+                                uint8_t* flags, float* omega_x, float* omega_y, void* stream) {
+    return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, flags, nullptr,
+                      stream, true, omega_x, omega_y, variant);
 }
 
 int bos_index_gradient(const float* phase, size_t n, double n0, double mu, double f_x, double cell_len,

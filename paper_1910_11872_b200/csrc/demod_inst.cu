@@ -12,7 +12,7 @@
 
 namespace bos {
 
-template <int M, bool COUNT>
+template <int M, bool COUNT, bool FB>
 cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
@@ -20,15 +20,19 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
     const dim3 grid((unsigned)((W + kBX - 1) / kBX), (unsigned)((H + kBY - 1) / kBY),
                     (unsigned)std::min(n_frames, 65535));
     if constexpr (M >= kWideMinM) {
-        demod_wide_kernel<M, COUNT><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
+        demod_wide_kernel<M, COUNT, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
     } else {
-        demod_kernel<M, COUNT><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
+        demod_kernel<M, COUNT, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
     }
     return cudaGetLastError();
 }
 
-template cudaError_t launch_demod<BOS_INST_M, false>(const float2*, int, int, int, const float*, float*, uint8_t*,
-                                                     float*, float*, unsigned long long*, cudaStream_t);
-template cudaError_t launch_demod<BOS_INST_M, true>(const float2*, int, int, int, const float*, float*, uint8_t*,
-                                                    float*, float*, unsigned long long*, cudaStream_t);
+#define BOS_INST(COUNT, FB)                                                                                  \
+    template cudaError_t launch_demod<BOS_INST_M, COUNT, FB>(const float2*, int, int, int, const float*, float*, \
+                                                             uint8_t*, float*, float*, unsigned long long*,   \
+                                                             cudaStream_t);
+BOS_INST(false, false)
+BOS_INST(true, false)
+BOS_INST(false, true)   // variant f4 (forward–backward averaging); no counting instance
+#undef BOS_INST
 }  // namespace bos

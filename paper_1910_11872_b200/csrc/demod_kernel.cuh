@@ -40,6 +40,17 @@ constexpr int kThreads = kBX * kBY;
 
 constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyond)
 constexpr float kPowerTol = 1e-8f;    // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2) ≤ 3.3e-4 where σ1²/σ2² ≥ 1.3)
+// NEWTON_STOP sweeps also require every Newton ratio |P/P′|² < tol2, not only every Aberth
+// step: an approximation repelled by its neighbours can take small steps far from any root
+// (the repulsion term balances P/P′), and the loose stop then misses the root it is heading
+// for.  Seen with the FB variant's polynomials (clamped border windows); always on there.
+// The paper path keeps the plain step test (−11 % throughput at 10 dB otherwise; DESIGN.md
+// §6 measures how often the two differ); BOS_STOP_NEWTON_PAPER=1 turns it on there too.
+#ifndef BOS_STOP_NEWTON_PAPER
+#define BOS_STOP_NEWTON_PAPER 0
+#endif
+template <bool FB>
+constexpr bool newton_stop() { return FB || BOS_STOP_NEWTON_PAPER != 0; }
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.032), then polish
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
@@ -175,7 +186,7 @@ __device__ __forceinline__ cx2 mirror(cx2 z) {
 // already-updated roots 0..k−1).  All register indices stay static; the I-cache holds one
 // root update.  Complex values are packed (cx2.cuh): Horner and the reciprocal sum run on
 // FFMA2.  Returns the number of sweeps; `ok` = converged or stagnated at FP32 noise.
-template <int N>
+template <int N, bool NEWTON_STOP = false>
 __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2], bool& ok, float tol2) {
     constexpr int K = N / 2;
     cx2 zm[K];
@@ -186,6 +197,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
     ok = false;
     for (; it < kAberthMaxIt; ++it) {
         float maxw = 0.0f;
+        bool parked = false;               // some |P/P′|² ≥ tol2 (NEWTON_STOP)
 #pragma unroll kSweepUnroll
         for (int r = 0; r < K; ++r) {
             const float2 zi = cx2_f2(z[0]);
@@ -225,6 +237,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
             }
             const cx2 zn = cx2_make(zi.x - w.x, zi.y - w.y);
             maxw = fmaxf(maxw, w2);
+            if (NEWTON_STOP && !near) parked |= !(cabs2(num) < tol2 * cabs2(den));   // near: the P′ step is the test
 #pragma unroll
             for (int j = 0; j + 1 < K; ++j) {
                 z[j] = z[j + 1];
@@ -233,7 +246,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
             z[K - 1] = zn;
             zm[K - 1] = mirror(zn);
         }
-        if (maxw < tol2) { ok = true; ++it; break; }
+        if (maxw < tol2 && !parked) { ok = true; ++it; break; }
     }
     return it;
 }
@@ -301,13 +314,152 @@ __device__ __forceinline__ float2 music_coeffs(const float2 (&q)[M], cx2 (&c)[2 
     return make_float2(r1.x * inv, -r1.y * inv);
 }
 
+// Sum of outer products of M-vectors drawn from the window: ROWS = false → the columns
+// Γ_w(:,k) (R = Γ_wΓ_w^H = R_y); ROWS = true → the rows Γ_w(i,:) (S = Σ_i row_i row_i^H =
+// conj(Γ_w^HΓ_w)).  Real diagonal Rd + strict lower triangle Ro;  R_ij += a_i·conj(a_j) =
+// re(a_j)·a_i + im(a_j)·(−j·a_i): two FFMA2 per entry.
+template <int M, int TW, bool ROWS>
+__device__ __forceinline__ void covariance(const float2* win, float (&Rd)[M], cx2 (&Ro)[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1]) {
+    constexpr int NOFF = M * (M - 1) / 2;
+#pragma unroll
+    for (int i = 0; i < M; ++i) Rd[i] = 0.0f;
+#pragma unroll
+    for (int t = 0; t < NOFF; ++t) Ro[t] = 0ull;
+    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+#pragma unroll 1
+    for (int k = 0; k < M; ++k) {   // rolled: one vector of Γ_w per trip (code size, regs)
+        cx2 col[M], colnj[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float2 g = ROWS ? win[k * TW + i] : win[i * TW + k];
+            col[i] = cx2_make(g.x, g.y);
+            colnj[i] = mul2(cx2_make(g.y, g.x), kPosNeg);     // −j·a = (im a, −re a)
+            Rd[i] = fmaf(g.x, g.x, fmaf(g.y, g.y, Rd[i]));
+        }
+#pragma unroll
+        for (int i = 1; i < M; ++i) {
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                cx2& r = Ro[tri_off<M>(i, j)];
+                r = fma2(cx2_bcast(cx2_re(col[j])), col[i], fma2(cx2_bcast(cx2_im(col[j])), colnj[i], r));
+            }
+        }
+    }
+}
+
+// Forward–backward average (variant f4, not in the paper): R ← ½(R + J conj(R) J), J the
+// exchange matrix:  R_ij ← ½(R_ij + conj(R_{M−1−i, M−1−j})) = ½(R_ij + R_{M−1−j, M−1−i}).
+template <int M>
+__device__ __forceinline__ void fb_average(float (&Rd)[M], cx2 (&Ro)[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1]) {
+    float d2[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) d2[i] = 0.5f * (Rd[i] + Rd[M - 1 - i]);
+#pragma unroll
+    for (int i = 0; i < M; ++i) Rd[i] = d2[i];
+    constexpr int NOFF = M * (M - 1) / 2;
+    cx2 o2[NOFF > 0 ? NOFF : 1];
+#pragma unroll
+    for (int i = 1; i < M; ++i) {
+#pragma unroll
+        for (int j = 0; j < i; ++j)
+            o2[tri_off<M>(i, j)] = mul2(add2(Ro[tri_off<M>(i, j)], Ro[tri_off<M>(M - 1 - j, M - 1 - i)]), cx2_bcast(0.5f));
+    }
+#pragma unroll
+    for (int t = 0; t < NOFF; ++t) Ro[t] = o2[t];
+}
+
+// Dominant eigenvector of the Hermitian R (Rd, Ro) by power iteration from the lag-1 tone
+// estimate u_i = e^{jω̂ i}, e^{jω̂} ∝ Σ_i R[i+1][i] (RAMP: u_i = (i − (M−1)/2)·e^{jω̂ i}, the
+// second start of the FB variant), normalised; stops at ‖u_{k+1} − u_k‖² < kPowerTol.
+// lam = ‖R u‖ of the last step (the Rayleigh quotient at convergence).
+template <int M, bool RAMP = false>
+__device__ __forceinline__ int power_iteration(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1],
+                                               cx2 (&u)[M], bool& ok, float& lam) {
+    float2 r1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
+    float2 e = make_float2(1.0f, 0.0f);
+    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+    {
+        // Σ_i (i − c)² = M(M²−1)/12
+        const float s0 = RAMP ? rsqrtf(float(M) * float(M * M - 1) / 12.0f) : rsqrtf(float(M));
+        float2 t = make_float2(1.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float wgt = RAMP ? s0 * (float(i) - 0.5f * float(M - 1)) : s0;
+            u[i] = cx2_make(wgt * t.x, wgt * t.y);
+            t = cmul(t, e);
+        }
+    }
+    lam = 0.0f;
+    ok = false;
+    int n = 0;
+    for (; n < kPowerMaxIt;) {
+        // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
+        cx2 uj[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
+        cx2 y[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                const cx2 r = Ro[tri_off<M>(i, j)];
+                acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
+            }
+#pragma unroll
+            for (int j = i + 1; j < M; ++j) {
+                const cx2 r = Ro[tri_off<M>(j, i)];
+                acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
+            }
+            y[i] = acc;
+        }
+        float nrm2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+        lam = sqrtf(nrm2);
+        float diff = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const cx2 yn = mul2(y[i], inv);
+            diff += cabs2(cx2_f2(sub2(yn, u[i])));
+            u[i] = yn;
+        }
+        ++n;
+        if (diff < kPowerTol) { ok = true; break; }
+    }
+    return n;
+}
+
+// Variant f4: the dominant eigenvector of a forward–backward averaged R.  The tone start can
+// be (numerically) orthogonal to it — FB splits a window's tones into conjugate-symmetric and
+// -antisymmetric combinations, e.g. on clamped border windows — and the step-size stop then
+// accepts the runner-up.  Two starts (tone, ramp-weighted tone); the larger ‖R u‖ wins.
+template <int M>
+__device__ __forceinline__ int power_iteration_fb(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1],
+                                                  cx2 (&u)[M], bool& ok) {
+    cx2 ua[M];
+    bool oka = false;
+    float l0, l1;
+    int n = power_iteration<M, false>(Rd, Ro, u, ok, l0);
+    n += power_iteration<M, true>(Rd, Ro, ua, oka, l1);
+    if (l1 > l0) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) u[i] = ua[i];
+        ok = oka;
+    }
+    return n;
+}
+
 // CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).
 template <int M>
 constexpr int min_blocks_per_sm() {
     return M <= 8 ? 4 : (M <= 10 ? 3 : (M <= 13 ? 2 : 1));
 }
 
-template <int M, bool COUNT>
+template <int M, bool COUNT, bool FB = false>
 __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<M>())
 demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
              const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
@@ -390,79 +542,94 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 fl |= kFlagNonfinite;
                 result = CUDART_NAN_F;
             } else {
-                // ---- a3: dominant eigenvector of R_y by power iteration ----
-                // start: u_i = e^{jω̂ i}/√M with e^{jω̂} ∝ Σ_i R[i+1][i] (lag-1 correlation)
-                float2 r1 = make_float2(0.0f, 0.0f);
-#pragma unroll
-                for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
-                float2 e = make_float2(1.0f, 0.0f);
-                if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
                 cx2 u[M];
-                {
-                    float2 t = make_float2(rsqrtf(float(M)), 0.0f);
-#pragma unroll
-                    for (int i = 0; i < M; ++i) {
-                        u[i] = cx2_make(t.x, t.y);
-                        t = cmul(t, e);
-                    }
-                }
                 bool pow_ok = false;
-                for (n_pow = 0; n_pow < kPowerMaxIt;) {
-                    // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
-                    cx2 uj[M];
-#pragma unroll
-                    for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
-                    cx2 y[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) {
-                        cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
-#pragma unroll
-                        for (int j = 0; j < i; ++j) {
-                            const cx2 r = Ro[tri_off<M>(i, j)];
-                            acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
-                        }
-#pragma unroll
-                        for (int j = i + 1; j < M; ++j) {
-                            const cx2 r = Ro[tri_off<M>(j, i)];
-                            acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
-                        }
-                        y[i] = acc;
-                    }
-                    float nrm2 = 0.0f;
-#pragma unroll
-                    for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
-                    const cx2 inv = cx2_bcast(rsqrtf(nrm2));
-                    float diff = 0.0f;
-#pragma unroll
-                    for (int i = 0; i < M; ++i) {
-                        const cx2 yn = mul2(y[i], inv);
-                        diff += cabs2(cx2_f2(sub2(yn, u[i])));
-                        u[i] = yn;
-                    }
-                    ++n_pow;
-                    if (diff < kPowerTol) { pow_ok = true; break; }
-                }
-                // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
-                cx2 unj[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) unj[i] = mul2(cx2_make(cx2_im(u[i]), cx2_re(u[i])), kPosNeg);
-                cx2 vp[M];
-                float vn = 0.0f;
-#pragma unroll
-                for (int k = 0; k < M; ++k) {
-                    cx2 acc = 0ull;
-#pragma unroll
-                    for (int i = 0; i < M; ++i) {
-                        const float2 g = win[i * TW + k];
-                        acc = fma2(cx2_bcast(g.x), u[i], fma2(cx2_bcast(g.y), unj[i], acc));
-                    }
-                    vp[k] = acc;
-                    vn += cabs2(cx2_f2(acc));
-                }
-                const cx2 vinv = cx2_bcast(rsqrtf(vn));
                 float2 v[M];
+                if constexpr (!FB) {
+                    // ---- a3: dominant eigenvector of R_y by power iteration ----
+                    // start: u_i = e^{jω̂ i}/√M with e^{jω̂} ∝ Σ_i R[i+1][i] (lag-1 correlation)
+                    float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int k = 0; k < M; ++k) v[k] = cx2_f2(mul2(vp[k], vinv));
+                    for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
+                    float2 e = make_float2(1.0f, 0.0f);
+                    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+                    {
+                        float2 t = make_float2(rsqrtf(float(M)), 0.0f);
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            u[i] = cx2_make(t.x, t.y);
+                            t = cmul(t, e);
+                        }
+                    }
+                    for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                        // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
+                        cx2 uj[M];
+#pragma unroll
+                        for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
+                        cx2 y[M];
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
+#pragma unroll
+                            for (int j = 0; j < i; ++j) {
+                                const cx2 r = Ro[tri_off<M>(i, j)];
+                                acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
+                            }
+#pragma unroll
+                            for (int j = i + 1; j < M; ++j) {
+                                const cx2 r = Ro[tri_off<M>(j, i)];
+                                acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
+                            }
+                            y[i] = acc;
+                        }
+                        float nrm2 = 0.0f;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+                        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+                        float diff = 0.0f;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            const cx2 yn = mul2(y[i], inv);
+                            diff += cabs2(cx2_f2(sub2(yn, u[i])));
+                            u[i] = yn;
+                        }
+                        ++n_pow;
+                        if (diff < kPowerTol) { pow_ok = true; break; }
+                    }
+                    // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
+                    cx2 unj[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) unj[i] = mul2(cx2_make(cx2_im(u[i]), cx2_re(u[i])), kPosNeg);
+                    cx2 vp[M];
+                    float vn = 0.0f;
+#pragma unroll
+                    for (int k = 0; k < M; ++k) {
+                        cx2 acc = 0ull;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            const float2 g = win[i * TW + k];
+                            acc = fma2(cx2_bcast(g.x), u[i], fma2(cx2_bcast(g.y), unj[i], acc));
+                        }
+                        vp[k] = acc;
+                        vn += cabs2(cx2_f2(acc));
+                    }
+                    const cx2 vinv = cx2_bcast(rsqrtf(vn));
+#pragma unroll
+                    for (int k = 0; k < M; ++k) v[k] = cx2_f2(mul2(vp[k], vinv));
+                } else {
+                    // variant f4 (not in the paper): dominant eigenvectors of the FB-averaged
+                    // R_y and of FB(S), S = Σ_i row_i row_i^H = conj(R_x); v_1 = conj(eigvec of FB(S))
+                    fb_average<M>(Rd, Ro);
+                    n_pow = power_iteration_fb<M>(Rd, Ro, u, pow_ok);
+                    covariance<M, TW, true>(win, Rd, Ro);
+                    fb_average<M>(Rd, Ro);
+                    cx2 sv[M];
+                    bool pow2_ok = false;
+                    n_pow += power_iteration_fb<M>(Rd, Ro, sv, pow2_ok);
+                    pow_ok = pow_ok && pow2_ok;
+#pragma unroll
+                    for (int k = 0; k < M; ++k) v[k] = cconj(cx2_f2(sv[k]));
+                }
                 float2 uf[M];
 #pragma unroll
                 for (int i = 0; i < M; ++i) uf[i] = cx2_f2(u[i]);
@@ -488,7 +655,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     float tol2 = kAberthTol2;
 #pragma unroll 1
                     for (int attempt = 0;; ++attempt) {
-                        its += aberth_sym<N>(c, z, ok, tol2);
+                        its += aberth_sym<N, newton_stop<FB>()>(c, z, ok, tol2);
                         zs = select_root<N / 2>(z, marg, z2);
                         // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
                         // ~1e-5 there); Newton steps on the selected root alone then make it

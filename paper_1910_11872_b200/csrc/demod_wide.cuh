@@ -132,13 +132,102 @@ __device__ __forceinline__ float2 newton_ratio_warp(const cx2* __restrict__ c, f
     return cdiv(num, den);
 }
 
+// Variant f4 (forward–backward averaging, not in the paper), lane i holding row i of the
+// Hermitian R:  R_ij ← ½(R_ij + conj(R_{M−1−i, M−1−j})).  Register j of lane M−1−i is R_{M−1−i, j},
+// so for a fixed register index every lane reads the same index from its mirror lane (one
+// shuffle per register); pairs (j, M−1−j) are updated together so no read sees a new value.
+template <int M>
+__device__ __forceinline__ void fb_average_rows(cx2 (&R)[M], int ri) {
+    const int src = M - 1 - ri;
+#pragma unroll
+    for (int j = 0; j < M / 2; ++j) {
+        const float2 a = cx2_f2(shfl_cx2(R[M - 1 - j], src));   // R_{M−1−i, M−1−j}
+        const float2 b = cx2_f2(shfl_cx2(R[j], src));           // R_{M−1−i, j}
+        R[j] = mul2(add2(R[j], f2_cx2(cconj(a))), cx2_bcast(0.5f));
+        R[M - 1 - j] = mul2(add2(R[M - 1 - j], f2_cx2(cconj(b))), cx2_bcast(0.5f));
+    }
+    if (M & 1) {
+        const float2 a = cx2_f2(shfl_cx2(R[M / 2], src));
+        R[M / 2] = mul2(add2(R[M / 2], f2_cx2(cconj(a))), cx2_bcast(0.5f));
+    }
+}
+
+// Dominant eigenvector of the Hermitian R (lane i: row i) by power iteration from the lag-1
+// tone estimate (as the thread kernel); lane i returns u_i (0 on lanes ≥ M).  `va` is the
+// warp's broadcast buffer.  Returns the iteration count; ok = converged.
+template <int M, bool RAMP = false>
+__device__ __forceinline__ int power_iteration_warp(const cx2 (&R)[M], int lane, bool rl, cx2* va, cx2& u, bool& ok,
+                                                    float& lam) {
+    const cx2 kNegPos = cx2_make(-1.0f, 1.0f);
+    float2 sub = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+        if (j + 1 == lane) sub = cx2_f2(R[j]);
+    const float2 r1 = warp_sum2(rl ? sub : make_float2(0.0f, 0.0f));   // Σ_i R[i+1][i]
+    float2 e = make_float2(1.0f, 0.0f);
+    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+    {
+        float2 t = make_float2(1.0f, 0.0f), ul = t;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            if (j == lane) ul = t;
+            t = cmul(t, e);
+        }
+        // RAMP (second FB start): weight (i − (M−1)/2); Σ_i (i − c)² = M(M²−1)/12
+        const float wgt = RAMP ? rsqrtf(float(M) * float(M * M - 1) / 12.0f) * (float(lane) - 0.5f * float(M - 1))
+                               : rsqrtf(float(M));
+        u = rl ? cx2_make(wgt * ul.x, wgt * ul.y) : 0ull;
+    }
+    ok = false;
+    lam = 0.0f;
+    int n = 0;
+    for (; n < kPowerMaxIt;) {
+        if (rl) va[lane] = u;
+        __syncwarp();
+        cx2 y = 0ull;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const cx2 uj = va[j];                                   // broadcast
+            const cx2 ujj = mul2(cx2_make(cx2_im(uj), cx2_re(uj)), kNegPos);
+            y = fma2(cx2_bcast(cx2_re(R[j])), uj, fma2(cx2_bcast(cx2_im(R[j])), ujj, y));
+        }
+        __syncwarp();
+        if (!rl) y = 0ull;
+        const float nrm2 = warp_sum(cabs2(cx2_f2(y)));
+        const cx2 yn = mul2(y, cx2_bcast(rsqrtf(nrm2)));
+        lam = sqrtf(nrm2);
+        const float diff = warp_sum(cabs2(cx2_f2(sub2(yn, u))));
+        u = yn;
+        ++n;
+        if (diff < kPowerTol) { ok = true; break; }
+    }
+    return n;
+}
+
+// Variant f4: two starts (tone, ramp-weighted tone), the larger ‖R u‖ wins (see the thread
+// kernel's power_iteration_fb for why one start is not enough under FB averaging).
+template <int M>
+__device__ __forceinline__ int power_iteration_warp_fb(const cx2 (&R)[M], int lane, bool rl, cx2* va, cx2& u,
+                                                       bool& ok) {
+    cx2 ua;
+    bool oka = false;
+    float l0, l1;
+    int n = power_iteration_warp<M, false>(R, lane, rl, va, u, ok, l0);
+    n += power_iteration_warp<M, true>(R, lane, rl, va, ua, oka, l1);
+    if (l1 > l0) {          // warp-uniform (warp sums)
+        u = ua;
+        ok = oka;
+    }
+    return n;
+}
+
 #ifndef BOS_WIDE_BLOCKS
 #define BOS_WIDE_BLOCKS 0
 #endif
 template <int M>
 constexpr int wide_min_blocks() { return BOS_WIDE_BLOCKS > 0 ? BOS_WIDE_BLOCKS : (M <= 24 ? 3 : 2); }
 
-template <int M, bool COUNT>
+template <int M, bool COUNT, bool FB = false>
 __global__ void __launch_bounds__(kThreads, wide_min_blocks<M>())
 demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                   const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
@@ -217,14 +306,11 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         R[j] = fma2(cx2_bcast(-bo.x), Ao, fma2(cx2_bcast(-bo.y), Aonj, R[j]));
                     }
                 }
-                // diagonal element R_ii and sub-diagonal R_{i,i−1} of this lane's row
+                // diagonal element R_ii of this lane's row
                 float dii = 0.0f;
-                float2 sub = make_float2(0.0f, 0.0f);
 #pragma unroll
-                for (int j = 0; j < M; ++j) {
+                for (int j = 0; j < M; ++j)
                     if (j == lane) dii = cx2_re(R[j]);
-                    if (j + 1 == lane) sub = cx2_f2(R[j]);
-                }
                 const float trace = warp_sum(rl ? dii : 0.0f);
 
                 uint8_t fl = 0;
@@ -232,58 +318,57 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     fl |= kFlagBorder;
                 float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
                 int n_pow = 0, n_aby = 0, n_abx = 0;
-                rebuild = !isfinite(trace);          // NaN/Inf never leave R by subtraction
+                // NaN/Inf never leave R by subtraction; the FB variant overwrites R (no slide)
+                rebuild = FB || !isfinite(trace);
                 if (!isfinite(trace)) {
                     fl |= kFlagNonfinite;
                     result = CUDART_NAN_F;
                 } else {
                     // ---- a3: power iteration, lane i holds u_i ----
-                    const float2 r1 = warp_sum2(rl ? sub : make_float2(0.0f, 0.0f));   // Σ_i R[i+1][i]
-                    float2 e = make_float2(1.0f, 0.0f);
-                    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+                    if (FB) fb_average_rows<M>(R, ri);
                     cx2 u;
-                    {
-                        float2 t = make_float2(rsqrtf(float(M)), 0.0f), ul = t;
-#pragma unroll
-                        for (int j = 0; j < M; ++j) {
-                            if (j == lane) ul = t;
-                            t = cmul(t, e);
-                        }
-                        u = rl ? cx2_make(ul.x, ul.y) : 0ull;
-                    }
                     bool pow_ok = false;
-                    for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                    if constexpr (FB) {
+                        n_pow = power_iteration_warp_fb<M>(R, lane, rl, va, u, pow_ok);
+                    } else {
+                        float lam;
+                        n_pow = power_iteration_warp<M>(R, lane, rl, va, u, pow_ok, lam);
+                    }
+                    cx2 v = 0ull;
+                    if (!FB) {
+                        // v_1 ∝ Γ_w^H u_1, lane k holds v_k
                         if (rl) va[lane] = u;
                         __syncwarp();
-                        cx2 y = 0ull;
 #pragma unroll
-                        for (int j = 0; j < M; ++j) {
-                            const cx2 uj = va[j];                                   // broadcast
-                            const cx2 ujj = mul2(cx2_make(cx2_im(uj), cx2_re(uj)), kNegPos);
-                            y = fma2(cx2_bcast(cx2_re(R[j])), uj, fma2(cx2_bcast(cx2_im(R[j])), ujj, y));
+                        for (int i = 0; i < M; ++i) {
+                            const float2 g = wrow[i * TW + p + ri];
+                            const cx2 ui = va[i];
+                            const cx2 uinj = mul2(cx2_make(cx2_im(ui), cx2_re(ui)), kPosNeg);
+                            v = fma2(cx2_bcast(g.x), ui, fma2(cx2_bcast(g.y), uinj, v));
                         }
-                        __syncwarp();
-                        if (!rl) y = 0ull;
-                        const float nrm2 = warp_sum(cabs2(cx2_f2(y)));
-                        const cx2 yn = mul2(y, cx2_bcast(rsqrtf(nrm2)));
-                        const float diff = warp_sum(cabs2(cx2_f2(sub2(yn, u))));
-                        u = yn;
-                        ++n_pow;
-                        if (diff < kPowerTol) { pow_ok = true; break; }
-                    }
-                    // v_1 ∝ Γ_w^H u_1, lane k holds v_k
-                    if (rl) va[lane] = u;
-                    __syncwarp();
-                    cx2 v = 0ull;
+                        if (!rl) v = 0ull;
+                        v = mul2(v, cx2_bcast(rsqrtf(warp_sum(cabs2(cx2_f2(v))))));
+                    } else {
+                        // variant f4: S = Σ_i row_i row_i^H = conj(Γ_w^H Γ_w), lane k holds row k:
+                        // S_kl = Σ_i Γ(i,k) conj(Γ(i,l)); v_1 = conj(dominant eigenvector of FB(S))
 #pragma unroll
-                    for (int i = 0; i < M; ++i) {
-                        const float2 g = wrow[i * TW + p + ri];
-                        const cx2 ui = va[i];
-                        const cx2 uinj = mul2(cx2_make(cx2_im(ui), cx2_re(ui)), kPosNeg);
-                        v = fma2(cx2_bcast(g.x), ui, fma2(cx2_bcast(g.y), uinj, v));
+                        for (int j = 0; j < M; ++j) R[j] = 0ull;
+#pragma unroll 1
+                        for (int i = 0; i < M; ++i) {
+                            const float2 g = wrow[i * TW + p + ri];
+                            const cx2 A = cx2_make(g.x, g.y), Anj = cx2_make(g.y, -g.x);
+#pragma unroll
+                            for (int j = 0; j < M; ++j) {
+                                const float2 b = wrow[i * TW + p + j];
+                                R[j] = fma2(cx2_bcast(b.x), A, fma2(cx2_bcast(b.y), Anj, R[j]));
+                            }
+                        }
+                        fb_average_rows<M>(R, ri);
+                        bool pow2_ok = false;
+                        n_pow += power_iteration_warp_fb<M>(R, lane, rl, va, v, pow2_ok);
+                        pow_ok = pow_ok && pow2_ok;
+                        v = f2_cx2(cconj(cx2_f2(v)));
                     }
-                    if (!rl) v = 0ull;
-                    v = mul2(v, cx2_bcast(rsqrtf(warp_sum(cabs2(cx2_f2(v))))));
                     __syncwarp();
 
                     // ---- a4 + a5 per axis ----
@@ -362,7 +447,8 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             z = csub(z, w);
                             zp = f2_cx2(z);
                             __syncwarp();                      // everyone has read va/vb
-                            if (warp_max(w2) < tol2) { ok = true; ++it; break; }
+                            const float n2 = (newton_stop<FB>() && kl && !near) ? cabs2(ratio) : 0.0f;   // see newton_stop
+                            if (warp_max(fmaxf(w2, n2 < 1e30f ? n2 : CUDART_INF_F)) < tol2) { ok = true; ++it; break; }
                         }
                         // selection: argmin |log2 |z|²| over lanes, margin to a different frequency
                         const float r2 = cabs2(z);

@@ -5,7 +5,7 @@
 #include <stdint.h>
 
 namespace bos {
-template <int M, bool COUNT>
+template <int M, bool COUNT, bool FB>
 cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s);

@@ -31,7 +31,17 @@ def main():
     ap.add_argument("--frames", type=int, default=8)
     ap.add_argument("--size", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--variant", default="paper", choices=["paper", "fb"],
+                    help="fb: row f4 forward-backward variant (timing + parity; no iteration counts)")
     args = ap.parse_args()
+    fb = args.variant == "fb"
+
+    def demod(frames_, M_, ref_=None, out_=None):
+        if fb:
+            return bosrm.bos_rootmusic_demod_variant(frames_, M_, variant=bosrm.VARIANT_FB, ref_phase=ref_,
+                                                     out_phase=out_)[:2]
+        return bosrm.bos_rootmusic_demod(frames_, M_, ref_phase=ref_, out_phase=out_)
+
     dev = torch.device("cuda", 0)
     w = synth.workload("C4", H=args.size, W=args.size)
     T = args.frames
@@ -42,33 +52,37 @@ def main():
     print("| M | Mpixel/s | frames/s at 2048² | power its | Aberth sweeps y/x | kflop/px | TFLOP/s | frac of 74.45 | parity rms / max (rad) |")
     print("|---|---|---|---|---|---|---|---|---|")
     for M in [int(x) for x in args.sizes.split(",")]:
-        ref, _ = bosrm.bos_rootmusic_demod(frames[0:1], M)
+        ref, _ = demod(frames[0:1], M)
         ref = ref[0].contiguous()
         out = torch.empty(T, w.H, w.W, dtype=torch.float32, device=dev)
-        bosrm.bos_rootmusic_demod(frames, M, ref_phase=ref, out_phase=out)
+        demod(frames, M, ref, out)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.reps):
-            bosrm.bos_rootmusic_demod(frames, M, ref_phase=ref, out_phase=out)
+            demod(frames, M, ref, out)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.reps
         mpx = T * plane / (ms / 1e3) / 1e6
-        cnt = bosrm.bos_rootmusic_iteration_counts(frames[1:2], M)
-        npx = cnt["pixels"]
-        kpi, ky, kx = cnt["power_its"] / npx, cnt["aberth_y"] / npx, cnt["aberth_x"] / npx
-        fpx = bench.flops_per_pixel(M, kpi, ky, kx)
+        if fb:
+            kpi = ky = kx = float("nan")
+            fpx = float("nan")
+        else:
+            cnt = bosrm.bos_rootmusic_iteration_counts(frames[1:2], M)
+            npx = cnt["pixels"]
+            kpi, ky, kx = cnt["power_its"] / npx, cnt["aberth_y"] / npx, cnt["aberth_x"] / npx
+            fpx = bench.flops_per_pixel(M, kpi, ky, kx)
         tf = fpx * mpx * 1e6 / 1e12
         rng = np.random.default_rng(M)
         pix = (rng.integers(0, w.H, 1024), rng.integers(0, w.W, 1024))
         host = frames[[0, T - 1]].cpu().numpy()
-        o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1])
+        o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1], variant=args.variant)
         g = out[T - 1].cpu().numpy()[pix]
         valid = (ofl[0] & R.PARITY_EXCLUDE_MASK) == 0
         e = R.wrap(g - o[0])[valid]
         rms, mx = float(math.sqrt(np.mean(e * e))), float(np.max(np.abs(e)))
-        row = dict(M=M, mpix_s=mpx, fps_2048=mpx / (plane / 1e6), power_its=kpi, aberth_y=ky, aberth_x=kx,
+        row = dict(M=M, variant=args.variant, mpix_s=mpx, fps_2048=mpx / (plane / 1e6), power_its=kpi, aberth_y=ky, aberth_x=kx,
                    kflop_px=fpx / 1e3, tflops=tf, frac=tf / peak, parity_rms=rms, parity_max=mx,
                    kernel="demod_kernel (thread/pixel)" if M <= 18 else "demod_wide_kernel (warp/pixel)")
         rows.append(row)
