@@ -20,6 +20,7 @@ from .rootmusic import (  # noqa: F401
     estimate_windows,
     extract_windows,
     index_gradient,
+    vertical_profile,
     music_polynomial,
     noise_projectors,
     select_root,

@@ -392,3 +392,17 @@ def rms_max_wrapped(a, b, valid=None):
 def index_gradient(phase, n0: float, mu: float, f_x: float, cell_len: float):
     """Eq.(17): ∂n/∂x = (1/(2 μ f_x)) · (n0 / L²) · φ, pointwise (FP64)."""
     return (1.0 / (2.0 * mu * f_x)) * (n0 / (cell_len * cell_len)) * np.asarray(phase, dtype=np.float64)
+
+
+def vertical_profile(phase):
+    """Row f3, SPEC ``stack_series``: per-frame vertical profile, the
+    column-averaged phase as a function of the row y (the paper's time-evolution comparison,
+    Figs. 6-8).  phase [..., H, W] → [..., H] (FP64); non-finite pixels are
+    skipped, a row without finite pixels gives NaN."""
+    p = np.asarray(phase, dtype=np.float64)
+    fin = np.isfinite(p)
+    n = fin.sum(axis=-1)
+    s = np.where(fin, p, 0.0).sum(axis=-1)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        return np.where(n > 0, s / np.maximum(n, 1), np.nan)
+

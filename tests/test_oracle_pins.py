@@ -410,3 +410,47 @@ def test_eq17_index_gradient_example():
     assert abs(base - 2 * 0.6665) < 1e-12
     assert abs(R.index_gradient(1.0, 1.333, 2.0, 1e4, 0.01) - 0.6665 / 2) < 1e-12
     assert abs(R.index_gradient(1.0, 1.333, 1.0, 1e4, 0.02) - 0.6665 / 4) < 1e-12
+
+
+def test_vertical_profile_closed_forms():
+    """Row f3 / SPEC stack_series: column-averaged φ per row.  Separable map
+    f(y) + g(x) with Σ_x g = 0 → exactly f; NaN pixels skipped; an all-NaN row → NaN;
+    identical frames → identical profiles."""
+    H, W = 17, 24
+    y = np.arange(H, dtype=np.float64)
+    x = np.arange(W, dtype=np.float64)
+    f = np.sin(0.3 * y) + 0.01 * y * y
+    g = np.cos(2 * np.pi * x / W)                       # sums to 0 over a full period
+    ph = f[:, None] + g[None, :]
+    assert np.allclose(R.vertical_profile(ph), f, atol=1e-12)
+    ph2 = ph.copy()
+    ph2[3, 5] = np.nan
+    ph2[4, :] = np.inf
+    prof = R.vertical_profile(ph2)
+    assert abs(prof[3] - (ph[3].sum() - ph[3, 5]) / (W - 1)) < 1e-12
+    assert np.isnan(prof[4])
+    st = np.stack([ph, ph])
+    p2 = R.vertical_profile(st)
+    assert p2.shape == (2, H) and np.array_equal(p2[0], p2[1])
+
+
+def test_vertical_profile_fick_phantom():
+    """SPEC S:L401 [DERIVED]: profiles of the Fick phase (∝ ∂c/∂y of the erfc step solution,
+    a Gaussian of variance 2Dt, Eq.(16)) at t = 120 s and 600 s: the peak falls by
+    √(600/120) and the width grows by the same factor."""
+    D, dy = 1.5e-9, 9.1e-6
+    H, W = 2001, 8
+    yy = (np.arange(H) - H // 2) * dy
+
+    def phi(t):
+        prof = np.exp(-yy * yy / (4 * D * t)) / np.sqrt(np.pi * D * t)
+        return np.repeat(prof[:, None], W, axis=1)
+
+    p1, p2 = R.vertical_profile(phi(120.0)), R.vertical_profile(phi(600.0))
+    assert abs(p1.max() / p2.max() - np.sqrt(5.0)) < 1e-9
+
+    def fwhm(p):
+        above = np.nonzero(p >= p.max() / 2)[0]
+        return (above[-1] - above[0]) * dy
+
+    assert abs(fwhm(p2) / fwhm(p1) - np.sqrt(5.0)) < 0.02
