@@ -182,6 +182,17 @@ int bos_index_gradient(const float* phase, size_t n, double n0, double mu, doubl
                        double cell_len, float* out, void* stream);
 
 /*
+ * bos_vertical_profile — SURVEY §8 row f3 ("diffusion profiles"; SPEC stack_series,
+ * S:L395-401): the per-frame vertical profile of a phase (or ∂n/∂x) stack, the mean over the
+ * columns x of every row y, for the paper's time-evolution comparison (Figs. 6-8).
+ *   phase  DEVICE float32 [n_frames][H][W].  Non-finite pixels are skipped; a row without
+ *          finite pixels gives NaN.  Accumulated in FP64, stored as float32.
+ *   out    DEVICE float32 [n_frames][H]; must not overlap `phase`.
+ * Returns BOS_ERR_INVALID_ARG for NULL/host pointers, non-positive sizes or overlap.
+ */
+int bos_vertical_profile(const float* phase, int n_frames, int H, int W, float* out, void* stream);
+
+/*
  * bos_analytic_signal — SURVEY §8 row f1, the step before the path: the analytic (complex)
  * fringe signal Γ of Eq.(1) from 8-bit intensity frames by "bandpass filtering and carrier
  * removal".  Per frame: I/255 → 2-D FFT → keep the disc of radius `radius`

@@ -52,6 +52,7 @@ SIGNATURES = {
                                  _SZ, _VP]),
     "bos_index_gradient": (_I, [_VP, _SZ, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                 _VP, _VP]),
+    "bos_vertical_profile": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "bos_strerror": (ctypes.c_char_p, [_I]),
     "bos_abi_version": (_I, []),
 }
@@ -280,6 +281,21 @@ def bos_index_gradient(phase: torch.Tensor, n0: float, mu: float, f_x: float, ce
                                   float(cell_len), out.data_ptr(), _stream_ptr(stream))
     _check(rc, "bos_index_gradient")
     return out
+
+
+def bos_vertical_profile(phase: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Row f3: column-averaged phase per row of a CUDA float32 [T,H,W] (or [H,W]) → [T,H] (or [H])."""
+    squeeze = phase.dim() == 2
+    ph = _dev_tensor(phase.unsqueeze(0) if squeeze else phase, torch.float32, "phase")
+    if ph.dim() != 3:
+        raise ValueError("phase must be [H,W] or [T,H,W]")
+    T, H, W = ph.shape
+    if out is None:
+        out = torch.empty(T, H, dtype=torch.float32, device=ph.device)
+    _dev_tensor(out, torch.float32, "out")
+    rc = lib().bos_vertical_profile(ph.data_ptr(), T, H, W, out.data_ptr(), _stream_ptr(stream))
+    _check(rc, "bos_vertical_profile")
+    return out[0] if squeeze and out.dim() == 2 and out.shape[0] == 1 else out
 
 
 def bos_analytic_signal(frames_u8: torch.Tensor, fx: float, fy: float, radius: float, remove_carrier: bool = False,

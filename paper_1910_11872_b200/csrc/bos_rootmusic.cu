@@ -2,6 +2,7 @@
 // dispatch, the time-lapse stack driver and the pipelined host-buffer driver.
 // The C ABI is declared (and documented) in include/bos_rootmusic.h.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -136,6 +137,33 @@ __global__ void index_gradient_kernel(const float* __restrict__ phase, size_t n,
     }
 }
 
+// Row f3, SPEC stack_series: column-averaged phase per row.  One warp per
+// (frame, row): coalesced lane-strided loads, FP64 sum and count of the finite pixels,
+// shuffle reduction.  HBM-bound (4 B read per pixel).
+__global__ void vertical_profile_kernel(const float* __restrict__ phase, size_t rows, int W,
+                                        float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const size_t warps = (size_t)gridDim.x * (blockDim.x >> 5);
+    for (size_t r = (size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+        const float* __restrict__ row = phase + r * (size_t)W;
+        double sum = 0.0;
+        int cnt = 0;
+        for (int x = lane; x < W; x += 32) {
+            const float v = __ldg(row + x);
+            if (isfinite(v)) {
+                sum += (double)v;
+                ++cnt;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) out[r] = cnt > 0 ? (float)(sum / (double)cnt) : CUDART_NAN_F;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -181,6 +209,16 @@ int bos_index_gradient(const float* phase, size_t n, double n0, double mu, doubl
     const double k = n0 / (2.0 * mu * f_x * cell_len * cell_len);
     const unsigned blocks = (unsigned)std::min<size_t>((n / 4 + 255) / 256 + 1, 148 * 16);
     index_gradient_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(phase, n, (float)k, out);
+    return cudaGetLastError() == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
+}
+
+int bos_vertical_profile(const float* phase, int n_frames, int H, int W, float* out, void* stream) {
+    if (phase == nullptr || out == nullptr || n_frames < 1 || H < 1 || W < 1) return BOS_ERR_INVALID_ARG;
+    const size_t rows = (size_t)n_frames * (size_t)H;
+    if (overlaps(phase, rows * (size_t)W * sizeof(float), out, rows * sizeof(float))) return BOS_ERR_INVALID_ARG;
+    if (!is_device_ptr(phase) || !is_device_ptr(out)) return BOS_ERR_INVALID_ARG;
+    const unsigned blocks = (unsigned)std::min<size_t>((rows + 7) / 8, 148 * 16);
+    vertical_profile_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(phase, rows, W, out);
     return cudaGetLastError() == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 

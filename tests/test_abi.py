@@ -112,6 +112,16 @@ def test_index_gradient_argument_errors(L):
     assert g(p, 4, 1.333, 1.0, -1.0, 0.01, p, None) == bosrm.BOS_ERR_INVALID_ARG
 
 
+def test_vertical_profile_argument_errors(L):
+    f = L.bos_vertical_profile
+    buf = ctypes.create_string_buffer(4096)
+    p = ctypes.addressof(buf)
+    assert f(None, 1, 4, 4, p, None) == bosrm.BOS_ERR_INVALID_ARG
+    assert f(p, 0, 4, 4, p + 2048, None) == bosrm.BOS_ERR_INVALID_ARG
+    assert f(p, 1, 4, 4, p + 8, None) == bosrm.BOS_ERR_INVALID_ARG          # overlap
+    assert f(p, 1, 4, 4, p + 2048, None) == bosrm.BOS_ERR_INVALID_ARG       # host pointers
+
+
 def test_analytic_signal_argument_errors(L):
     f = L.bos_analytic_signal
     buf = ctypes.create_string_buffer(4096)

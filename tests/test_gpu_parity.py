@@ -316,6 +316,30 @@ def test_index_gradient_kernel():
     assert np.allclose(x.cpu().numpy(), R.index_gradient(ref.cpu().numpy(), 1.333, 1.0, 1e4, 0.01), rtol=1e-6)
 
 
+def test_vertical_profile_kernel():
+    """Row f3 profile: GPU vs the oracle's FP64 column mean on a demodulated C3 stack with NaN
+    pixels and one all-NaN row; ragged widths (not multiples of 32)."""
+    w = synth.workload("C3", H=96, W=77)
+    st = synth.make_stack(w, frames=range(4)).to(DEV)
+    ph, _, _ = bosrm.bos_rootmusic_demod_stack(st, 8, ref_index=0)
+    ph[1, 10, 3] = float("nan")
+    ph[2, 20, :] = float("inf")
+    prof = bosrm.bos_vertical_profile(ph)
+    torch.cuda.synchronize()
+    expect = R.vertical_profile(ph.cpu().numpy())
+    got = prof.cpu().numpy()
+    assert got.shape == (4, 96)
+    assert np.isnan(got[2, 20]) and np.isnan(expect[2, 20])
+    fin = np.isfinite(expect)
+    assert np.all(np.isfinite(got[fin]))
+    assert np.max(np.abs(got[fin] - expect[fin])) <= 1e-6 * max(1.0, np.max(np.abs(expect[fin])))
+    for W in (1, 31, 33, 1000):
+        x = torch.randn(3, 5, W, dtype=torch.float32, device=DEV)
+        g = bosrm.bos_vertical_profile(x)
+        torch.cuda.synchronize()
+        assert np.allclose(g.cpu().numpy(), R.vertical_profile(x.cpu().numpy()), rtol=1e-6, atol=1e-6)
+
+
 @pytest.mark.parametrize("M", [5, 8, 17, 24])
 def test_outputs_do_not_write_outside_their_buffers(M):
     """Canary guard bands around out / flags / ω buffers (compute-sanitizer is not available on
