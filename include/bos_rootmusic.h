@@ -54,7 +54,7 @@ enum {
 enum {
     BOS_FLAG_NONCONVERGED = 1 << 0,  /* eigen/root iteration cap hit, or no finite root */
     BOS_FLAG_AMBIGUOUS = 1 << 1,     /* two distinct-frequency root pairs within 1e-3 in |ln|z|| */
-    BOS_FLAG_SMALL_GAP = 1 << 2,     /* (oracle only) σ1²/σ2² < 1.3 */
+    BOS_FLAG_SMALL_GAP = 1 << 2,     /* (oracle and BOS_VARIANT_FP64 only) σ1²/σ2² < 1.3 */
     BOS_FLAG_LOW_AMPLITUDE = 1 << 3, /* |Σ Γ_w e^{-j(...)}| < 1e-4 · M · ‖Γ_w‖_F */
     BOS_FLAG_NONFINITE = 1 << 4,     /* window has NaN/Inf; output is NaN */
     BOS_FLAG_BORDER = 1 << 5         /* informational: window clamped at the frame edge */
@@ -66,10 +66,11 @@ enum {
 #define BOS_WINDOW_LEN_MAX 32
 #define BOS_MODEL_ORDER 3   /* Eq.(3): φ_w = α + ω_x x + ω_y y, three parameters [R3] */
 
-/* Covariance variants for bos_rootmusic_demod_variant. */
+/* Variants for bos_rootmusic_demod_variant: a bit mask. */
 enum {
-    BOS_VARIANT_PAPER = 0,  /* Algorithm 1 as published: singular vectors of Γ_w */
-    BOS_VARIANT_FB = 1      /* NOT in the paper: forward–backward averaged covariances, see below */
+    BOS_VARIANT_PAPER = 0,  /* Algorithm 1 as published: singular vectors of Γ_w, FP32 */
+    BOS_VARIANT_FB = 1,     /* NOT in the paper: forward–backward averaged covariances, see below */
+    BOS_VARIANT_FP64 = 2    /* NOT in the paper (its GPU code is FP32): the whole pixel in double */
 };
 
 /*
@@ -153,13 +154,21 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W,
 /*
  * bos_rootmusic_demod_variant — bos_rootmusic_demod_ex with a selectable covariance
  * (a standard root-MUSIC extension the paper does NOT use; the paper's
- * Algorithm 1 is variant BOS_VARIANT_PAPER, identical to bos_rootmusic_demod_ex).
+ * Algorithm 1 is variant BOS_VARIANT_PAPER, identical to bos_rootmusic_demod_ex).  The
+ * FP32 variants run the kernels of the hot path; FP64 runs demod_f64.cuh.
  *   variant  BOS_VARIANT_PAPER: u_1, v_1 = dominant singular vectors of Γ_w (Algorithm 1 l.4).
  *            BOS_VARIANT_FB: u_1 = dominant eigenvector of ½(R_y + J R_y* J), R_y = Γ_wΓ_w^H,
  *            v_1 = dominant eigenvector of ½(R_x + J R_x* J), R_x = Γ_w^HΓ_w (J: the M×M
  *            exchange matrix; the backward snapshots J·conj(column)).  Both are exact for the
  *            Eq.(3) plane-wave model; the rest of Algorithm 1 (Eqs.(12),(13), root selection,
- *            Eq.(15)) is unchanged.  Any other value: BOS_ERR_UNSUPPORTED.
+ *            Eq.(15)) is unchanged.
+ *            BOS_VARIANT_FP64 (alone or | BOS_VARIANT_FB): every step in double precision —
+ *            Jacobi eigen-decompositions of R_y and R_x, Aberth on all 2M−2 roots to the
+ *            rounding bound, Eq.(15) in double; outputs are still float32.  Also sets
+ *            BOS_FLAG_SMALL_GAP (λ1/λ2 < 1.3; for FB the smaller of the two axes').  Built
+ *            for accuracy, not speed (thread-local matrices: ≈50 KB local memory per thread
+ *            at M = 32).
+ *            Any other value: BOS_ERR_UNSUPPORTED.
  * Other arguments, errors and determinism as bos_rootmusic_demod_ex.
  */
 int bos_rootmusic_demod_variant(const bos_cf32* frames, int n_frames, int H, int W,

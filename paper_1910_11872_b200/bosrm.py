@@ -34,6 +34,7 @@ MODEL_ORDER = 3
 
 VARIANT_PAPER = 0   # Algorithm 1 as published
 VARIANT_FB = 1      # row f4: forward–backward averaged covariances (not in the paper)
+VARIANT_FP64 = 2    # row f4: the whole pixel in double precision (bit mask, combinable with FB)
 
 # name -> (restype, argtypes); must match include/bos_rootmusic.h
 _VP, _I, _SZ = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t

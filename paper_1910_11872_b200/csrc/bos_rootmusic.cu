@@ -52,6 +52,46 @@ LaunchFn pick(int M) {
         default: return nullptr;
     }
 }
+
+using LaunchF64 = cudaError_t (*)(const float2*, int, int, int, const float*, float*, uint8_t*, float*, float*,
+                                  cudaStream_t);
+
+template <bool FB>
+LaunchF64 pick_f64(int M) {
+    switch (M) {
+        case 3: return bos::launch_demod_f64<3, FB>;
+        case 4: return bos::launch_demod_f64<4, FB>;
+        case 5: return bos::launch_demod_f64<5, FB>;
+        case 6: return bos::launch_demod_f64<6, FB>;
+        case 7: return bos::launch_demod_f64<7, FB>;
+        case 8: return bos::launch_demod_f64<8, FB>;
+        case 9: return bos::launch_demod_f64<9, FB>;
+        case 10: return bos::launch_demod_f64<10, FB>;
+        case 11: return bos::launch_demod_f64<11, FB>;
+        case 12: return bos::launch_demod_f64<12, FB>;
+        case 13: return bos::launch_demod_f64<13, FB>;
+        case 14: return bos::launch_demod_f64<14, FB>;
+        case 15: return bos::launch_demod_f64<15, FB>;
+        case 16: return bos::launch_demod_f64<16, FB>;
+        case 17: return bos::launch_demod_f64<17, FB>;
+        case 18: return bos::launch_demod_f64<18, FB>;
+        case 19: return bos::launch_demod_f64<19, FB>;
+        case 20: return bos::launch_demod_f64<20, FB>;
+        case 21: return bos::launch_demod_f64<21, FB>;
+        case 22: return bos::launch_demod_f64<22, FB>;
+        case 23: return bos::launch_demod_f64<23, FB>;
+        case 24: return bos::launch_demod_f64<24, FB>;
+        case 25: return bos::launch_demod_f64<25, FB>;
+        case 26: return bos::launch_demod_f64<26, FB>;
+        case 27: return bos::launch_demod_f64<27, FB>;
+        case 28: return bos::launch_demod_f64<28, FB>;
+        case 29: return bos::launch_demod_f64<29, FB>;
+        case 30: return bos::launch_demod_f64<30, FB>;
+        case 31: return bos::launch_demod_f64<31, FB>;
+        case 32: return bos::launch_demod_f64<32, FB>;
+        default: return nullptr;
+    }
+}
 static_assert(BOS_WINDOW_LEN_MAX <= BOS_TEMPLATE_M_MAX, "template table too small");
 
 // 1 if p is a device (or managed) pointer, 0 otherwise.
@@ -105,8 +145,15 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
         if (ref_phase != nullptr && !is_device_ptr(ref_phase)) return BOS_ERR_INVALID_ARG;
         if (flags != nullptr && !is_device_ptr(flags)) return BOS_ERR_INVALID_ARG;
     }
-    if (variant != BOS_VARIANT_PAPER && variant != BOS_VARIANT_FB) return BOS_ERR_UNSUPPORTED;
-    if (variant == BOS_VARIANT_FB && counters != nullptr) return BOS_ERR_UNSUPPORTED;
+    if ((variant & ~(BOS_VARIANT_FB | BOS_VARIANT_FP64)) != 0) return BOS_ERR_UNSUPPORTED;
+    if (variant != BOS_VARIANT_PAPER && counters != nullptr) return BOS_ERR_UNSUPPORTED;
+    if (variant & BOS_VARIANT_FP64) {
+        LaunchF64 f = (variant & BOS_VARIANT_FB) ? pick_f64<true>(window_len) : pick_f64<false>(window_len);
+        if (f == nullptr) return BOS_ERR_UNSUPPORTED;
+        const cudaError_t e = f(reinterpret_cast<const float2*>(frames), n_frames, H, W, ref_phase, out_phase, flags,
+                                omega_x, omega_y, static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
+    }
     LaunchFn fn = variant == BOS_VARIANT_FB ? pick<false, true>(window_len)
                                             : (counters ? pick<true, false>(window_len) : pick<false, false>(window_len));
     if (fn == nullptr) return BOS_ERR_UNSUPPORTED;

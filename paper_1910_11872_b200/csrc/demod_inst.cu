@@ -2,6 +2,7 @@
 // M = BOS_INST_M (the build compiles this file once per M, in parallel).
 #include <algorithm>
 
+#include "demod_f64.cuh"
 #include "demod_kernel.cuh"
 #include "demod_wide.cuh"
 #include "launch.h"
@@ -26,6 +27,19 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
     }
     return cudaGetLastError();
 }
+
+template <int M, bool FB>
+cudaError_t launch_demod_f64(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+                             uint8_t* flags, float* omega_x, float* omega_y, cudaStream_t s) {
+    const dim3 block(32, 4, 1);
+    const dim3 grid((unsigned)((W + 31) / 32), (unsigned)((H + 3) / 4), (unsigned)std::min(n_frames, 65535));
+    f64::demod_f64_kernel<M, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y);
+    return cudaGetLastError();
+}
+template cudaError_t launch_demod_f64<BOS_INST_M, false>(const float2*, int, int, int, const float*, float*,
+                                                         uint8_t*, float*, float*, cudaStream_t);
+template cudaError_t launch_demod_f64<BOS_INST_M, true>(const float2*, int, int, int, const float*, float*,
+                                                        uint8_t*, float*, float*, cudaStream_t);
 
 #define BOS_INST(COUNT, FB)                                                                                  \
     template cudaError_t launch_demod<BOS_INST_M, COUNT, FB>(const float2*, int, int, int, const float*, float*, \

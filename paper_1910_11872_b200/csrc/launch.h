@@ -9,4 +9,8 @@ template <int M, bool COUNT, bool FB>
 cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s);
+// row f4: the FP64 path (demod_f64.cuh)
+template <int M, bool FB>
+cudaError_t launch_demod_f64(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+                             uint8_t* flags, float* omega_x, float* omega_y, cudaStream_t s);
 }  // namespace bos

@@ -31,14 +31,17 @@ def main():
     ap.add_argument("--frames", type=int, default=8)
     ap.add_argument("--size", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--variant", default="paper", choices=["paper", "fb"],
-                    help="fb: row f4 forward-backward variant (timing + parity; no iteration counts)")
+    ap.add_argument("--variant", default="paper", choices=["paper", "fb", "fp64", "fb_fp64"],
+                    help="row f4 variants (timing + parity vs the oracle of the same variant; no iteration counts)")
     args = ap.parse_args()
-    fb = args.variant == "fb"
+    fb = args.variant != "paper"
+    vbits = {"paper": 0, "fb": bosrm.VARIANT_FB, "fp64": bosrm.VARIANT_FP64,
+             "fb_fp64": bosrm.VARIANT_FB | bosrm.VARIANT_FP64}[args.variant]
+    ovar = "fb" if args.variant.startswith("fb") else "paper"
 
     def demod(frames_, M_, ref_=None, out_=None):
         if fb:
-            return bosrm.bos_rootmusic_demod_variant(frames_, M_, variant=bosrm.VARIANT_FB, ref_phase=ref_,
+            return bosrm.bos_rootmusic_demod_variant(frames_, M_, variant=vbits, ref_phase=ref_,
                                                      out_phase=out_)[:2]
         return bosrm.bos_rootmusic_demod(frames_, M_, ref_phase=ref_, out_phase=out_)
 
@@ -77,7 +80,7 @@ def main():
         rng = np.random.default_rng(M)
         pix = (rng.integers(0, w.H, 1024), rng.integers(0, w.W, 1024))
         host = frames[[0, T - 1]].cpu().numpy()
-        o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1], variant=args.variant)
+        o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1], variant=ovar)
         g = out[T - 1].cpu().numpy()[pix]
         valid = (ofl[0] & R.PARITY_EXCLUDE_MASK) == 0
         e = R.wrap(g - o[0])[valid]
