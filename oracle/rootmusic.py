@@ -22,7 +22,8 @@ The oracle follows Algorithm 1 literally, for every pixel independe
 plus the time-lapse reference difference wrap(φ_t − φ_ref) (BASELINE north_star, [R7]).
 Variant "fb" (NOT in the paper, [R13]): line 4 uses the eigenvectors of the
 forward–backward averaged covariances instead of the SVD (fb_subspaces); everything else is
-unchanged.
+unchanged.  ``subarray_len`` m < M (row f4, [R14]): line 4 uses the eigenvectors of the
+spatially smoothed covariances of order m (ss_covariances, degree-(2m−2) polynomials).
 Library primitives used as single steps: ``numpy.linalg.svd`` (LAPACK zgesdd) for the SVD
 and ``numpy.linalg.eigvals`` (LAPACK zgeev: balancing + Hessenberg + shifted QR) for the
 companion-matrix eigenvalues.  No blocking, fusion or reordering beyond the paper's steps.
@@ -136,6 +137,38 @@ def fb_subspaces(win: np.ndarray):
     return U, S, np.conj(np.swapaxes(V, 1, 2)), Sx
 
 
+def ss_covariances(win: np.ndarray, m: int):
+    """Spatially smoothed (reduced-order) covariances of order m ≤ M (variant f4, NOT in the
+    paper; Shan, Wax & Kailath 1985): the snapshots of R_y are all length-m segments of the
+    columns of Γ_w, x_{s,k} = Γ_w[s:s+m, k]; those of R_x are the conjugated length-m segments
+    of the rows, y_{s,i} = conj(Γ_w[i, s:s+m]) (so that m = M gives Γ_wΓ_w^H and Γ_w^HΓ_w):
+        R_y = Σ_{s=0}^{M−m} Σ_k x_{s,k} x_{s,k}^H,   R_x = Σ_{s=0}^{M−m} Σ_i y_{s,i} y_{s,i}^H."""
+    N, M, _ = win.shape
+    if not 2 <= m <= M:
+        raise ValueError("subarray length must be in [2, M]")
+    Ry = np.zeros((N, m, m), dtype=np.complex128)
+    Rx = np.zeros((N, m, m), dtype=np.complex128)
+    for s in range(M - m + 1):
+        X = win[:, s:s + m, :]                                  # columns = snapshots
+        Y = np.swapaxes(np.conj(win[:, :, s:s + m]), 1, 2)      # [N, m, M]: columns = conj rows
+        Ry += X @ np.conj(np.swapaxes(X, 1, 2))
+        Rx += Y @ np.conj(np.swapaxes(Y, 1, 2))
+    return Ry, Rx
+
+
+def eig_subspaces(Ry: np.ndarray, Rx: np.ndarray, fb: bool = False):
+    """Eigenvectors (descending) of the two axes' covariances, optionally FB-averaged; returned
+    like fb_subspaces: (U, S, V^H, S_x) with S = √λ(R_y), S_x = √λ(R_x)."""
+    if fb:
+        Ry, Rx = fb_average(Ry), fb_average(Rx)
+    ly, U = np.linalg.eigh(Ry)
+    lx, V = np.linalg.eigh(Rx)
+    U, V = U[:, :, ::-1], V[:, :, ::-1]
+    S = np.sqrt(np.maximum(ly[:, ::-1], 0.0))
+    Sx = np.sqrt(np.maximum(lx[:, ::-1], 0.0))
+    return U, S, np.conj(np.swapaxes(V, 1, 2)), Sx
+
+
 VARIANTS = ("paper", "fb")
 
 
@@ -242,16 +275,21 @@ def selection_margin(roots: np.ndarray, z_sel: np.ndarray) -> np.ndarray:
         return other.min(axis=1) - d_sel
 
 
-def estimate_windows(win: np.ndarray, variant: str = "paper"):
+def estimate_windows(win: np.ndarray, variant: str = "paper", subarray_len: int | None = None):
     """Algorithm 1 lines 4-11 on a batch of windows [N,M,M] (complex128, finite).
-    variant "fb" (row f4, not in the paper) replaces line 4 by fb_subspaces.
+    Row f4 (not in the paper): variant "fb" replaces line 4 by fb_subspaces; subarray_len
+    m < M replaces it by the eigenvectors of the spatially smoothed covariances of order m
+    (ss_covariances; polynomials of degree 2m−2; FB-averaged too for "fb").  Eq.(15) always
+    uses the whole M×M window.
 
     Returns dict: alpha (Eq.(15) phase), omega_x, omega_y, flags (bits 0-3), plus the
     intermediate z_y, z_x, S, margins for tests."""
     N, M, _ = win.shape
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
-    if variant == "paper":
+    if subarray_len is not None and subarray_len != M:
+        U, S, Vh, Sx = eig_subspaces(*ss_covariances(win, int(subarray_len)), fb=variant == "fb")
+    elif variant == "paper":
         U, S, Vh = svd_subspaces(win)
         Sx = S                       # one spectrum: σ of Γ_w serves both axes
     else:
@@ -296,11 +334,11 @@ def default_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
-def _estimate_pixels(frame, py, px, M, variant="paper"):
+def _estimate_pixels(frame, py, px, M, variant="paper", subarray_len=None):
     win, border = extract_windows(frame, py, px, M)
     finite = np.isfinite(win.real).all(axis=(1, 2)) & np.isfinite(win.imag).all(axis=(1, 2))
     safe = np.where(finite[:, None, None], win, 0.0)
-    res = estimate_windows(safe, variant)
+    res = estimate_windows(safe, variant, subarray_len)
     alpha = np.where(finite, res["alpha"], np.nan)
     flags = res["flags"].copy()
     flags[~finite] = FLAG_NONFINITE
@@ -309,7 +347,8 @@ def _estimate_pixels(frame, py, px, M, variant="paper"):
 
 
 def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_phase=None,
-                pixels=None, threads: int | None = None, chunk: int | None = None, variant: str = "paper"):
+                pixels=None, threads: int | None = None, chunk: int | None = None, variant: str = "paper",
+                subarray_len: int | None = None):
     """Phase map of one frame: Algorithm 1 at every pixel (or at ``pixels=(py, px)``).
 
     ref_phase: None → raw α (wrapped); else out = wrap(α - ref_phase) [R7], where
@@ -340,7 +379,7 @@ def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_ph
 
     def work(j):
         s, e = bounds[j], bounds[j + 1]
-        alpha[s:e], flags[s:e] = _estimate_pixels(frame, py[s:e], px[s:e], M, variant)
+        alpha[s:e], flags[s:e] = _estimate_pixels(frame, py[s:e], px[s:e], M, variant, subarray_len)
 
     if nthreads == 1 or len(bounds) <= 2:
         for j in range(len(bounds) - 1):
@@ -359,7 +398,8 @@ def demod_frame(frame: np.ndarray, window_len: int, model_order: int = 3, ref_ph
 
 
 def demod_stack(frames: np.ndarray, window_len: int, model_order: int = 3, ref_index: int = 0,
-                pixels=None, frame_indices=None, threads: int | None = None, variant: str = "paper"):
+                pixels=None, frame_indices=None, threads: int | None = None, variant: str = "paper",
+                subarray_len: int | None = None):
     """Time-lapse stack [T,H,W]: φ_ref = α(frames[ref_index]); out[t] = wrap(α_t - φ_ref).
 
     ``frame_indices`` restricts the output to those frames (sampled parity on big stacks);
@@ -369,10 +409,11 @@ def demod_stack(frames: np.ndarray, window_len: int, model_order: int = 3, ref_i
     T = frames.shape[0]
     ts = range(T) if frame_indices is None else frame_indices
     ref, ref_flags = demod_frame(frames[ref_index], window_len, model_order, None, pixels, threads,
-                                 variant=variant)
+                                 variant=variant, subarray_len=subarray_len)
     outs, fls = [], []
     for t in ts:
-        a, f = demod_frame(frames[t], window_len, model_order, None, pixels, threads, variant=variant)
+        a, f = demod_frame(frames[t], window_len, model_order, None, pixels, threads, variant=variant,
+                           subarray_len=subarray_len)
         outs.append(wrap(a - ref))
         fls.append(f | ref_flags)
     return np.stack(outs), np.stack(fls)

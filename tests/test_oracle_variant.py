@@ -158,3 +158,97 @@ def test_demod_frame_variant_threading():
     a1, f1 = R.demod_frame(f, 5, variant="fb", threads=1)
     a2, f2 = R.demod_frame(f, 5, variant="fb", threads=4)
     assert np.array_equal(a1, a2) and np.array_equal(f1, f2)
+
+
+# --------------------------------------------------------------------------------------
+# Spatial smoothing (subarray_len m < M), row f4 [R14]
+# --------------------------------------------------------------------------------------
+def test_ss_full_order_is_the_plain_covariance():
+    """m = M: one subarray, the snapshots are the columns / conjugated rows → Γ_wΓ_w^H and
+    Γ_w^HΓ_w exactly, whose top eigenvectors are the SVD's u_1, v_1."""
+    win = noisy_windows(7, 8, 21)
+    Ry, Rx = R.ss_covariances(win, 7)
+    Wh = np.conj(np.swapaxes(win, 1, 2))
+    assert np.allclose(Ry, win @ Wh, atol=1e-12) and np.allclose(Rx, Wh @ win, atol=1e-12)
+    U, S, Vh, Sx = R.eig_subspaces(Ry, Rx)
+    U2, S2, Vh2 = R.svd_subspaces(win)
+    assert np.allclose(np.abs(np.einsum("ni,ni->n", np.conj(U[:, :, 0]), U2[:, :, 0])), 1.0, atol=1e-9)
+    assert np.allclose(np.abs(np.einsum("ni,ni->n", Vh[:, 0, :], np.conj(Vh2[:, 0, :]))), 1.0, atol=1e-9)
+    assert np.allclose(S, S2, rtol=1e-9) and np.allclose(Sx, S2, rtol=1e-9)
+
+
+@pytest.mark.parametrize("M,m", [(8, 6), (11, 7), (16, 5)])
+def test_ss_decorrelates_coherent_waves(M, m):
+    """The textbook property of spatial smoothing (Shan, Wax & Kailath 1985): two coherent
+    tones along y (identical in every column) give a rank-1 R_y, but a rank-2 smoothed R_y
+    whose signal subspace contains both length-m steering vectors."""
+    o = R.window_offsets(M)
+    w1, w2 = 0.7, -0.4
+    col = np.exp(1j * w1 * o) + 0.8 * np.exp(1j * (w2 * o + 0.3))
+    win = np.repeat(col[:, None], M, axis=1)[None]
+    lam_full = np.linalg.eigvalsh(win[0] @ np.conj(win[0]).T)[::-1]
+    assert lam_full[1] < 1e-9 * lam_full[0]
+    Ry, _ = R.ss_covariances(win, m)
+    lam, U = np.linalg.eigh(Ry[0])
+    lam, U = lam[::-1], U[:, ::-1]
+    assert lam[1] > 1e-3 * lam[0] and lam[2] < 1e-9 * lam[0]
+    Un = U[:, 2:]
+    for w in (w1, w2):
+        a = np.exp(1j * w * np.arange(m))
+        assert np.linalg.norm(np.conj(Un).T @ a) < 1e-6 * np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("M,m", [(5, 3), (8, 3), (8, 5), (12, 8), (17, 9), (32, 16)])
+def test_ss_plane_wave_exact(M, m):
+    rng = np.random.default_rng(10 * M + m)
+    n = 16
+    wx = rng.uniform(-2.5, 2.5, n)
+    wy = rng.uniform(-2.5, 2.5, n)
+    a = rng.uniform(-math.pi, math.pi, n)
+    o = R.window_offsets(M)
+    win = np.exp(1j * (wx[:, None, None] * o[None, None, :] + wy[:, None, None] * o[None, :, None]
+                       + a[:, None, None]))
+    for variant in ("paper", "fb"):
+        r = R.estimate_windows(win, variant, subarray_len=m)
+        assert np.max(np.abs(r["omega_x"] - wx)) < 1e-6
+        assert np.max(np.abs(r["omega_y"] - wy)) < 1e-6
+        tol = 1e-9 if M % 2 else 1e-6
+        assert np.max(np.abs(R.wrap(r["alpha"] - a))) < tol
+        assert not np.any(r["flags"] & R.PARITY_EXCLUDE_MASK)
+
+
+def test_ss_m3_noise_free_roots_closed_form():
+    """m = 3 on a noise-free plane wave: the quartic's roots are the M = 3 template's
+    {e^{jω} (double), −(2 ∓ √3)e^{jω}} (pinned in test_oracle_pins for Eq.(12) at M = 3)."""
+    M, w = 9, 0.6
+    o = R.window_offsets(M)
+    win = np.exp(1j * (0.2 * o[None, :] + w * o[:, None]))[None]
+    Ry, Rx = R.ss_covariances(win, 3)
+    U, S, Vh, Sx = R.eig_subspaces(Ry, Rx)
+    Cy, _ = R.noise_projectors(U, Vh)
+    roots, _ = R.companion_roots(R.music_polynomial(Cy))
+    expect = np.array([np.exp(1j * w), np.exp(1j * w), -(2 - math.sqrt(3)) * np.exp(1j * w),
+                       -(2 + math.sqrt(3)) * np.exp(1j * w)])
+    got = np.sort_complex(roots[0])
+    for e in expect:
+        assert np.min(np.abs(got - e)) < 1e-6
+
+
+@pytest.mark.parametrize("M,m", [(8, 5), (11, 3)])
+def test_ss_metamorphic(M, m):
+    win = noisy_windows(M, 64, 800 + M)
+    base = R.estimate_windows(win, "paper", subarray_len=m)
+    ok = (base["flags"] & R.PARITY_EXCLUDE_MASK) == 0
+    assert ok.mean() > 0.8
+    tr = R.estimate_windows(np.swapaxes(win, 1, 2).copy(), "paper", subarray_len=m)
+    assert np.max(np.abs(R.wrap(tr["alpha"] - base["alpha"]))[ok]) < 1e-9
+    assert np.max(np.abs(R.wrap(tr["omega_x"] - base["omega_y"]))[ok]) < 1e-9
+    cj = R.estimate_windows(np.conj(win), "paper", subarray_len=m)
+    assert np.max(np.abs(R.wrap(cj["alpha"] + base["alpha"]))[ok]) < 1e-9
+    sh = R.estimate_windows(2.5 * np.exp(0.77j) * win, "paper", subarray_len=m)
+    assert np.max(np.abs(R.wrap(sh["alpha"] - base["alpha"] - 0.77))[ok]) < 1e-9
+
+
+def test_ss_rejects_bad_order():
+    with pytest.raises(ValueError):
+        R.ss_covariances(noisy_windows(5, 1, 0), 6)
