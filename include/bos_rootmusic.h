@@ -54,7 +54,7 @@ enum {
 enum {
     BOS_FLAG_NONCONVERGED = 1 << 0,  /* eigen/root iteration cap hit, or no finite root */
     BOS_FLAG_AMBIGUOUS = 1 << 1,     /* two distinct-frequency root pairs within 1e-3 in |ln|z|| */
-    BOS_FLAG_SMALL_GAP = 1 << 2,     /* (oracle and BOS_VARIANT_FP64 only) σ1²/σ2² < 1.3 */
+    BOS_FLAG_SMALL_GAP = 1 << 2,     /* (oracle and BOS_VARIANT_FP64 only) λ1/λ2 = σ1²/σ2² < 1.3 */
     BOS_FLAG_LOW_AMPLITUDE = 1 << 3, /* |Σ Γ_w e^{-j(...)}| < 1e-4 · M · ‖Γ_w‖_F */
     BOS_FLAG_NONFINITE = 1 << 4,     /* window has NaN/Inf; output is NaN */
     BOS_FLAG_BORDER = 1 << 5         /* informational: window clamped at the frame edge */
@@ -152,27 +152,34 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W,
                            void* stream);
 
 /*
- * bos_rootmusic_demod_variant — bos_rootmusic_demod_ex with a selectable covariance
- * (a standard root-MUSIC extension the paper does NOT use; the paper's
- * Algorithm 1 is variant BOS_VARIANT_PAPER, identical to bos_rootmusic_demod_ex).  The
- * FP32 variants run the kernels of the hot path; FP64 runs demod_f64.cuh.
- *   variant  BOS_VARIANT_PAPER: u_1, v_1 = dominant singular vectors of Γ_w (Algorithm 1 l.4).
- *            BOS_VARIANT_FB: u_1 = dominant eigenvector of ½(R_y + J R_y* J), R_y = Γ_wΓ_w^H,
- *            v_1 = dominant eigenvector of ½(R_x + J R_x* J), R_x = Γ_w^HΓ_w (J: the M×M
- *            exchange matrix; the backward snapshots J·conj(column)).  Both are exact for the
- *            Eq.(3) plane-wave model; the rest of Algorithm 1 (Eqs.(12),(13), root selection,
- *            Eq.(15)) is unchanged.
+ * bos_rootmusic_demod_variant — bos_rootmusic_demod_ex with the variants of SURVEY §8 row f4,
+ * standard root-MUSIC extensions the paper does NOT use (its Algorithm 1 is variant
+ * BOS_VARIANT_PAPER with subarray_len 0, identical to bos_rootmusic_demod_ex).
+ *   subarray_len  0 (or window_len): covariances of order M = window_len (Algorithm 1).
+ *            3 ≤ m < M: spatially smoothed covariances of order m ([R14]): R_y = Σ over all
+ *            length-m segments x of the window's columns of x x^H, R_x likewise over the
+ *            conjugated length-m segments of its rows; the polynomials have degree 2m − 2
+ *            (m = 3: a quartic, solved in closed form); Eq.(15) still uses the M×M window.
+ *            FP32: m ≤ 16 (BOS_ERR_UNSUPPORTED above); FP64: any m ≤ M.  m < 3 or m > M:
+ *            BOS_ERR_INVALID_ARG.
+ *   variant  bit mask.  BOS_VARIANT_FB: u_1 = dominant eigenvector of ½(R_y + J R_y* J),
+ *            v_1 = dominant eigenvector of ½(R_x + J R_x* J), R_y = Γ_wΓ_w^H,
+ *            R_x = Γ_w^HΓ_w (or their order-m versions; J: the exchange matrix; the backward
+ *            snapshots J·conj(x)).  Exact for the Eq.(3) plane-wave model; the rest of
+ *            Algorithm 1 (Eqs.(12),(13), root selection, Eq.(15)) is unchanged.
  *            BOS_VARIANT_FP64 (alone or | BOS_VARIANT_FB): every step in double precision —
- *            Jacobi eigen-decompositions of R_y and R_x, Aberth on all 2M−2 roots to the
+ *            Jacobi eigen-decompositions of R_y and R_x, Aberth on all 2m−2 roots to the
  *            rounding bound, Eq.(15) in double; outputs are still float32.  Also sets
- *            BOS_FLAG_SMALL_GAP (λ1/λ2 < 1.3; for FB the smaller of the two axes').  Built
- *            for accuracy, not speed (thread-local matrices: ≈50 KB local memory per thread
- *            at M = 32).
- *            Any other value: BOS_ERR_UNSUPPORTED.
- * Other arguments, errors and determinism as bos_rootmusic_demod_ex.
+ *            BOS_FLAG_SMALL_GAP (λ1/λ2 < 1.3; with FB or smoothing the smaller of the two
+ *            axes').  Built for accuracy, not speed (thread-local matrices: ≈50 KB local
+ *            memory per thread at M = 32).
+ *            Any other bit: BOS_ERR_UNSUPPORTED.
+ * The FP32 variants run the hot path's kernels (demod_kernel.cuh, demod_wide.cuh; smoothing:
+ * demod_ss.cuh); FP64 runs demod_f64.cuh.  Other arguments, errors and determinism as
+ * bos_rootmusic_demod_ex.
  */
 int bos_rootmusic_demod_variant(const bos_cf32* frames, int n_frames, int H, int W,
-                                int window_len, int model_order, int variant,
+                                int window_len, int subarray_len, int model_order, int variant,
                                 const float* ref_phase, float* out_phase, uint8_t* flags,
                                 float* omega_x, float* omega_y, void* stream);
 

@@ -45,7 +45,7 @@ SIGNATURES = {
     "bos_rootmusic_demod_stack_host": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _SZ, _I, _VP]),
     "bos_rootmusic_iteration_counts": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP]),
     "bos_rootmusic_demod_ex": (_I, [_VP, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
-    "bos_rootmusic_demod_variant": (_I, [_VP, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "bos_rootmusic_demod_variant": (_I, [_VP, _I, _I, _I, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     "bos_analytic_signal_workspace_bytes": (_SZ, [_I, _I, _I]),
     "bos_unwrap_workspace_bytes": (_SZ, [_I, _I, _I]),
     "bos_unwrap": (_I, [_VP, _I, _I, _I, _VP, _VP, _SZ, _VP]),
@@ -249,8 +249,10 @@ def bos_rootmusic_demod_ex(frames: torch.Tensor, window_len: int = 8, model_orde
 
 def bos_rootmusic_demod_variant(frames: torch.Tensor, window_len: int = 8, model_order: int = MODEL_ORDER,
                                 variant: int = VARIANT_FB, ref_phase: torch.Tensor | None = None,
-                                out_phase: torch.Tensor | None = None, flags=None, omega=False, stream=None):
-    """bos_rootmusic_demod_ex with a covariance variant (VARIANT_PAPER / VARIANT_FB)
+                                out_phase: torch.Tensor | None = None, flags=None, omega=False, stream=None,
+                                subarray_len: int = 0):
+    """bos_rootmusic_demod_ex with the row-f4 variants: ``variant`` a mask of VARIANT_FB /
+    VARIANT_FP64, ``subarray_len`` m < window_len for spatial smoothing (0 = none)
     → (phase, flags|None, ω_x|None, ω_y|None)."""
     frames = _dev_tensor(_frames3(frames), torch.complex64, "frames")
     T, H, W = frames.shape
@@ -263,7 +265,7 @@ def bos_rootmusic_demod_variant(frames: torch.Tensor, window_len: int = 8, model
     if ref_phase is not None:
         _dev_tensor(ref_phase, torch.float32, "ref_phase")
     rc = lib().bos_rootmusic_demod_variant(
-        frames.data_ptr(), T, H, W, int(window_len), int(model_order), int(variant),
+        frames.data_ptr(), T, H, W, int(window_len), int(subarray_len), int(model_order), int(variant),
         ref_phase.data_ptr() if ref_phase is not None else None, out.data_ptr(),
         fl.data_ptr() if fl is not None else None, wx.data_ptr() if wx is not None else None,
         wy.data_ptr() if wy is not None else None, _stream_ptr(stream))

@@ -53,8 +53,29 @@ LaunchFn pick(int M) {
     }
 }
 
-using LaunchF64 = cudaError_t (*)(const float2*, int, int, int, const float*, float*, uint8_t*, float*, float*,
+using LaunchF64 = cudaError_t (*)(const float2*, int, int, int, int, const float*, float*, uint8_t*, float*, float*,
                                   cudaStream_t);
+
+template <bool FB>
+LaunchF64 pick_ss(int MS) {
+    switch (MS) {
+        case 3: return bos::launch_demod_ss<3, FB>;
+        case 4: return bos::launch_demod_ss<4, FB>;
+        case 5: return bos::launch_demod_ss<5, FB>;
+        case 6: return bos::launch_demod_ss<6, FB>;
+        case 7: return bos::launch_demod_ss<7, FB>;
+        case 8: return bos::launch_demod_ss<8, FB>;
+        case 9: return bos::launch_demod_ss<9, FB>;
+        case 10: return bos::launch_demod_ss<10, FB>;
+        case 11: return bos::launch_demod_ss<11, FB>;
+        case 12: return bos::launch_demod_ss<12, FB>;
+        case 13: return bos::launch_demod_ss<13, FB>;
+        case 14: return bos::launch_demod_ss<14, FB>;
+        case 15: return bos::launch_demod_ss<15, FB>;
+        case 16: return bos::launch_demod_ss<16, FB>;
+        default: return nullptr;
+    }
+}
 
 template <bool FB>
 LaunchF64 pick_f64(int M) {
@@ -120,7 +141,7 @@ int check_common(int n_frames, int H, int W, int window_len, int model_order) {
 int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_len, int model_order,
                const float* ref_phase, float* out_phase, uint8_t* flags, unsigned long long* counters,
                void* stream, bool check_ptrs, float* omega_x = nullptr, float* omega_y = nullptr,
-               int variant = BOS_VARIANT_PAPER) {
+               int variant = BOS_VARIANT_PAPER, int subarray_len = 0) {
     int rc = check_common(n_frames, H, W, window_len, model_order);
     if (rc != BOS_OK) return rc;
     if (frames == nullptr || out_phase == nullptr) return BOS_ERR_INVALID_ARG;
@@ -146,12 +167,22 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
         if (flags != nullptr && !is_device_ptr(flags)) return BOS_ERR_INVALID_ARG;
     }
     if ((variant & ~(BOS_VARIANT_FB | BOS_VARIANT_FP64)) != 0) return BOS_ERR_UNSUPPORTED;
-    if (variant != BOS_VARIANT_PAPER && counters != nullptr) return BOS_ERR_UNSUPPORTED;
+    const int m = (subarray_len == 0) ? window_len : subarray_len;
+    if (m < BOS_WINDOW_LEN_MIN || m > window_len) return BOS_ERR_INVALID_ARG;
+    if ((variant != BOS_VARIANT_PAPER || m != window_len) && counters != nullptr) return BOS_ERR_UNSUPPORTED;
+    const bool fb = (variant & BOS_VARIANT_FB) != 0;
     if (variant & BOS_VARIANT_FP64) {
-        LaunchF64 f = (variant & BOS_VARIANT_FB) ? pick_f64<true>(window_len) : pick_f64<false>(window_len);
+        LaunchF64 f = fb ? pick_f64<true>(window_len) : pick_f64<false>(window_len);
         if (f == nullptr) return BOS_ERR_UNSUPPORTED;
-        const cudaError_t e = f(reinterpret_cast<const float2*>(frames), n_frames, H, W, ref_phase, out_phase, flags,
+        const cudaError_t e = f(reinterpret_cast<const float2*>(frames), n_frames, H, W, m, ref_phase, out_phase, flags,
                                 omega_x, omega_y, static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
+    }
+    if (m != window_len) {                       // FP32 spatial smoothing: order m ≤ 16
+        LaunchF64 f = fb ? pick_ss<true>(m) : pick_ss<false>(m);
+        if (f == nullptr) return BOS_ERR_UNSUPPORTED;
+        const cudaError_t e = f(reinterpret_cast<const float2*>(frames), n_frames, H, W, window_len, ref_phase,
+                                out_phase, flags, omega_x, omega_y, static_cast<cudaStream_t>(stream));
         return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
     }
     LaunchFn fn = variant == BOS_VARIANT_FB ? pick<false, true>(window_len)
@@ -241,10 +272,10 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W, i
 }
 
 int bos_rootmusic_demod_variant(const bos_cf32* frames, int n_frames, int H, int W, int window_len,
-                                int model_order, int variant, const float* ref_phase, float* out_phase,
-                                uint8_t* flags, float* omega_x, float* omega_y, void* stream) {
+                                int subarray_len, int model_order, int variant, const float* ref_phase,
+                                float* out_phase, uint8_t* flags, float* omega_x, float* omega_y, void* stream) {
     return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase, out_phase, flags, nullptr,
-                      stream, true, omega_x, omega_y, variant);
+                      stream, true, omega_x, omega_y, variant, subarray_len);
 }
 
 int bos_index_gradient(const float* phase, size_t n, double n0, double mu, double f_x, double cell_len,

@@ -6,7 +6,8 @@
 //
 //   a1  Γ_w: M×M clamped window [R1], promoted to double;
 //   a2  R_y = Γ_wΓ_w^H and R_x = Γ_w^HΓ_w (Eq.(4) and its x counterpart; the eigenvectors of
-//       these are the SVD's U and V), optionally forward–backward averaged (FB, [R13]);
+//       these are the SVD's U and V), or their spatially smoothed order-m versions
+//       ([R14]), optionally forward–backward averaged (FB, [R13]);
 //   a3  cyclic complex Jacobi eigen-decomposition of each (rotations until the off-diagonal
 //       norm is below 1e-15 of the Frobenius norm) → u_1, v_1 = eigenvectors of the largest
 //       eigenvalue, and λ1/λ2 for the SMALL_GAP flag (the FP32 kernels cannot emit it);
@@ -50,31 +51,35 @@ constexpr int kAberthMaxIt = 500;
 constexpr double kEps = 1.1102230246251565e-16;
 constexpr double kTauSel = 1e-3, kTauOmega = 1e-2, kGammaMin = 1.3, kLowAmp = 1e-4;
 
-// R ← Γ Γ^H (ROWS = false: R_ij = Σ_k Γ(i,k) conj(Γ(j,k))) or Γ^H Γ (ROWS = true: R_kl =
-// Σ_i conj(Γ(i,k)) Γ(i,l)); full Hermitian storage, row-major.
+// Covariance of order m ≤ M from the window g (M×M, row-major), full Hermitian storage
+// (row-major m×m).  ROWS = false: R_y = Σ_{s,k} x x^H with x = Γ[s:s+m, k] (m = M: Γ Γ^H);
+// ROWS = true: R_x = Σ_{s,i} y y^H with y = conj(Γ[i, s:s+m]) (m = M: Γ^H Γ).  m < M is the
+// spatially smoothed covariance of row f4 ([R14]).
 template <int M, bool ROWS>
-__device__ void gram(const cd* __restrict__ g, cd* __restrict__ R) {
+__device__ void gram(const cd* __restrict__ g, int m, cd* __restrict__ R) {
 #pragma unroll 1
-    for (int a = 0; a < M; ++a) {
+    for (int a = 0; a < m; ++a) {
 #pragma unroll 1
         for (int b = 0; b <= a; ++b) {
             cd s = mk(0.0, 0.0);
+#pragma unroll 1
+            for (int o = 0; o + m <= M; ++o) {
 #pragma unroll 4
-            for (int t = 0; t < M; ++t) {
-                const cd x = ROWS ? cj(g[t * M + a]) : g[a * M + t];
-                const cd y = ROWS ? cj(g[t * M + b]) : g[b * M + t];
-                s = add(s, mul(x, cj(y)));
+                for (int t = 0; t < M; ++t) {
+                    const cd x = ROWS ? cj(g[t * M + o + a]) : g[(o + a) * M + t];
+                    const cd y = ROWS ? cj(g[t * M + o + b]) : g[(o + b) * M + t];
+                    s = add(s, mul(x, cj(y)));
+                }
             }
-            R[a * M + b] = s;
-            R[b * M + a] = cj(s);
+            R[a * m + b] = s;
+            R[b * m + a] = cj(s);
         }
-        R[a * M + a].im = 0.0;
+        R[a * m + a].im = 0.0;
     }
 }
 
 // Forward–backward average ½(R + J R* J): R_ij ← ½(R_ij + conj(R_{M−1−i, M−1−j})).
-template <int M>
-__device__ void fb_average(cd* R) {
+__device__ inline void fb_average(cd* R, int M) {
 #pragma unroll 1
     for (int i = 0; i < M; ++i) {
 #pragma unroll 1
@@ -92,8 +97,7 @@ __device__ void fb_average(cd* R) {
 // Cyclic Jacobi for a Hermitian R (destroyed: diagonal → eigenvalues); V ← eigenvectors in
 // columns.  Each rotation: phase column/row q so that R_pq = |R_pq| is real, then the real
 // symmetric rotation t = sgn(θ)/(|θ| + √(θ²+1)), θ = (R_qq − R_pp)/(2|R_pq|).
-template <int M>
-__device__ bool jacobi(cd* R, cd* V) {
+__device__ inline bool jacobi(cd* R, cd* V, int M) {
 #pragma unroll 1
     for (int i = 0; i < M * M; ++i) V[i] = mk(0.0, 0.0);
 #pragma unroll 1
@@ -155,8 +159,7 @@ __device__ bool jacobi(cd* R, cd* V) {
 }
 
 // Column of V with the largest eigenvalue → q (normalised); gap = λ1/λ2 (∞ if λ2 ≤ 0).
-template <int M>
-__device__ void top_eigvec(const cd* R, const cd* V, cd* q, double& gap) {
+__device__ inline void top_eigvec(const cd* R, const cd* V, int M, cd* q, double& gap) {
     int b = 0;
 #pragma unroll 1
     for (int i = 1; i < M; ++i)
@@ -173,8 +176,7 @@ __device__ void top_eigvec(const cd* R, const cd* V, cd* q, double& gap) {
 
 // Eqs.(12),(13): c_{M−1} = M − ‖q‖², c_{M−1+d} = −r_d, c_{M−1−d} = −conj(r_d),
 // r_d = Σ_i q_i conj(q_{i+d}) (ascending powers); rot = conj(r_1)/|r_1| (template rotation).
-template <int M>
-__device__ cd coefficients(const cd* q, cd* c) {
+__device__ inline cd coefficients(const cd* q, int M, cd* c) {
     double n2 = 0.0;
 #pragma unroll 1
     for (int i = 0; i < M; ++i) n2 += abs2(q[i]);
@@ -194,15 +196,14 @@ __device__ cd coefficients(const cd* q, cd* c) {
 
 // All N roots of Σ c_k z^k: Gauss–Seidel Aberth–Ehrlich from the rotated template; a root is
 // frozen when |P(z)| ≤ 4Nε·Σ|c_k||z|^k.  Returns false at the iteration cap.
-template <int N>
-__device__ bool aberth_all(const cd* c, cd* z, int toff, cd rot) {
+__device__ inline bool aberth_all(const cd* c, int N, cd* z, int toff, cd rot) {
 #pragma unroll 1
     for (int k = 0; k < N; ++k) {
         const float2 t = kTemplateRoots[toff + k];
         z[k] = mul(mk(t.x, t.y), rot);
     }
     uint64_t frozen = 0;
-    const uint64_t all = (N >= 64) ? ~0ull : ((1ull << N) - 1ull);
+    const uint64_t all = (N >= 64) ? ~0ull : ((1ull << N) - 1ull);   // N ≤ 62
 #pragma unroll 1
     for (int it = 0; it < kAberthMaxIt; ++it) {
 #pragma unroll 1
@@ -237,8 +238,7 @@ __device__ bool aberth_all(const cd* c, cd* z, int toff, cd rot) {
 
 // argmin |ln|z||; margin = min over roots of a different frequency (|wrap(arg − arg_sel)| > τ_ω)
 // of |ln|z|| − |ln|z_sel|| ([R6], [R8]).
-template <int N>
-__device__ cd select(const cd* z, double& margin) {
+__device__ inline cd select(const cd* z, int N, double& margin) {
     int b = -1;
     double best = CUDART_INF;
 #pragma unroll 1
@@ -264,15 +264,14 @@ __device__ cd select(const cd* z, double& margin) {
 // Local storage per thread: window M², two matrices M², coefficients, roots.
 template <int M, bool FB>
 __global__ void __launch_bounds__(128)
-demod_f64_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, const float* __restrict__ ref,
+demod_f64_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int m, const float* __restrict__ ref,
                  float* __restrict__ out, uint8_t* __restrict__ flags, float* __restrict__ omx,
                  float* __restrict__ omy) {
-    constexpr int N = 2 * M - 2;
     constexpr int O0 = (M - 1) / 2;              // o_i = i − O0 [R2]
     const int px = blockIdx.x * 32 + threadIdx.x, py = blockIdx.y * 4 + threadIdx.y;
     if (px >= W || py >= H) return;
     const size_t plane = (size_t)H * (size_t)W;
-    cd g[M * M], A[M * M], V[M * M], c[N + 1], z[N], u[M], v[M];   // 50 KB at M = 32
+    cd g[M * M], A[M * M], V[M * M], c[2 * M - 1], z[2 * M - 2], u[M], v[M];   // 50 KB at M = 32
     for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
         const float2* __restrict__ frame = frames + (size_t)f * plane;
         uint8_t fl = 0;
@@ -296,31 +295,32 @@ demod_f64_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, 
         if (!finite) {
             fl |= 1u << 4;
         } else {
-            // ---- a2 + a3 ----
+            // ---- a2 + a3 (order m covariances; m = M is Algorithm 1 line 4) ----
             double gap_y, gap_x;
-            gram<M, false>(g, A);
-            if (FB) fb_average<M>(A);
-            bool ok = jacobi<M>(A, V);
-            top_eigvec<M>(A, V, u, gap_y);
-            gram<M, true>(g, A);
-            if (FB) fb_average<M>(A);
-            ok = jacobi<M>(A, V) && ok;
-            top_eigvec<M>(A, V, v, gap_x);
-            // ---- a4 + a5 per axis ----
+            gram<M, false>(g, m, A);
+            if (FB) fb_average(A, m);
+            bool ok = jacobi(A, V, m);
+            top_eigvec(A, V, m, u, gap_y);
+            gram<M, true>(g, m, A);
+            if (FB) fb_average(A, m);
+            ok = jacobi(A, V, m) && ok;
+            top_eigvec(A, V, m, v, gap_x);
+            // ---- a4 + a5 per axis (degree 2m − 2) ----
+            const int N = 2 * m - 2;
             cd zsel[2];
             double marg = CUDART_INF;
 #pragma unroll 1
             for (int axis = 0; axis < 2; ++axis) {
-                const cd rot = coefficients<M>(axis ? v : u, c);
-                ok = aberth_all<N>(c, z, bos_template_offset(M), rot) && ok;
-                double m;
-                zsel[axis] = select<N>(z, m);
-                marg = fmin(marg, m);
+                const cd rot = coefficients(axis ? v : u, m, c);
+                ok = aberth_all(c, N, z, bos_template_offset(m), rot) && ok;
+                double mg;
+                zsel[axis] = select(z, N, mg);
+                marg = fmin(marg, mg);
             }
             const cd zy = zsel[0], zx = zsel[1];
             if (!ok || !isfinite(zy.re + zy.im + zx.re + zx.im)) fl |= 1u << 0;
             if (marg < kTauSel) fl |= 1u << 1;
-            if (fmin(gap_y, FB ? gap_x : gap_y) < kGammaMin) fl |= 1u << 2;
+            if (fmin(gap_y, (FB || m < M) ? gap_x : gap_y) < kGammaMin) fl |= 1u << 2;
             // ---- a6: Eq.(15); ẑ_x = e^{−jω_x}, ẑ_y = e^{jω_y} ----
             const cd hx = scl(zx, 1.0 / sqrt(abs2(zx))), hy = scl(zy, 1.0 / sqrt(abs2(zy)));
             cd qy = mk(1.0, 0.0), tx0 = mk(1.0, 0.0);

@@ -4,6 +4,7 @@
 
 #include "demod_f64.cuh"
 #include "demod_kernel.cuh"
+#include "demod_ss.cuh"
 #include "demod_wide.cuh"
 #include "launch.h"
 
@@ -29,17 +30,38 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
 }
 
 template <int M, bool FB>
-cudaError_t launch_demod_f64(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+cudaError_t launch_demod_f64(const float2* frames, int n_frames, int H, int W, int m, const float* ref, float* out,
                              uint8_t* flags, float* omega_x, float* omega_y, cudaStream_t s) {
     const dim3 block(32, 4, 1);
     const dim3 grid((unsigned)((W + 31) / 32), (unsigned)((H + 3) / 4), (unsigned)std::min(n_frames, 65535));
-    f64::demod_f64_kernel<M, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y);
+    f64::demod_f64_kernel<M, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, m, ref, out, flags, omega_x, omega_y);
     return cudaGetLastError();
 }
-template cudaError_t launch_demod_f64<BOS_INST_M, false>(const float2*, int, int, int, const float*, float*,
+template cudaError_t launch_demod_f64<BOS_INST_M, false>(const float2*, int, int, int, int, const float*, float*,
                                                          uint8_t*, float*, float*, cudaStream_t);
-template cudaError_t launch_demod_f64<BOS_INST_M, true>(const float2*, int, int, int, const float*, float*,
+template cudaError_t launch_demod_f64<BOS_INST_M, true>(const float2*, int, int, int, int, const float*, float*,
                                                         uint8_t*, float*, float*, cudaStream_t);
+
+#if BOS_INST_M <= 16
+// row f4: spatially smoothed covariance of order MS = BOS_INST_M, runtime window M ≥ MS
+template <int MS, bool FB>
+cudaError_t launch_demod_ss(const float2* frames, int n_frames, int H, int W, int M, const float* ref, float* out,
+                            uint8_t* flags, float* omega_x, float* omega_y, cudaStream_t s) {
+    const size_t smem = (size_t)kBY * M * (kBX + M - 1) * sizeof(float2);
+    cudaError_t e = cudaFuncSetAttribute(ss::demod_ss_kernel<MS, FB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    const dim3 block(kBX, kBY, 1);
+    const dim3 grid((unsigned)((W + kBX - 1) / kBX), (unsigned)((H + kBY - 1) / kBY),
+                    (unsigned)std::min(n_frames, 65535));
+    ss::demod_ss_kernel<MS, FB><<<grid, block, smem, s>>>(frames, n_frames, H, W, M, ref, out, flags, omega_x, omega_y);
+    return cudaGetLastError();
+}
+template cudaError_t launch_demod_ss<BOS_INST_M, false>(const float2*, int, int, int, int, const float*, float*,
+                                                        uint8_t*, float*, float*, cudaStream_t);
+template cudaError_t launch_demod_ss<BOS_INST_M, true>(const float2*, int, int, int, int, const float*, float*,
+                                                       uint8_t*, float*, float*, cudaStream_t);
+#endif
 
 #define BOS_INST(COUNT, FB)                                                                                  \
     template cudaError_t launch_demod<BOS_INST_M, COUNT, FB>(const float2*, int, int, int, const float*, float*, \

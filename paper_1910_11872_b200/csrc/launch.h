@@ -11,6 +11,10 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
                          cudaStream_t s);
 // row f4: the FP64 path (demod_f64.cuh)
 template <int M, bool FB>
-cudaError_t launch_demod_f64(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+cudaError_t launch_demod_f64(const float2* frames, int n_frames, int H, int W, int m, const float* ref, float* out,
                              uint8_t* flags, float* omega_x, float* omega_y, cudaStream_t s);
+// row f4: spatially smoothed covariance of order MS ≤ 16, runtime window M (demod_ss.cuh)
+template <int MS, bool FB>
+cudaError_t launch_demod_ss(const float2* frames, int n_frames, int H, int W, int M, const float* ref, float* out,
+                            uint8_t* flags, float* omega_x, float* omega_y, cudaStream_t s);
 }  // namespace bos

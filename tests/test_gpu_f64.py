@@ -100,7 +100,7 @@ def test_f64_nonfinite_zero_and_errors():
     out = torch.empty(1, H, W, dtype=torch.float32, device=DEV)
     L = bosrm.lib()
     s = torch.cuda.current_stream().cuda_stream
-    assert L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, 8, 3, 4, None, out.data_ptr(), None, None, None,
+    assert L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, 8, 0, 3, 4, None, out.data_ptr(), None, None, None,
                                          s) == bosrm.BOS_ERR_UNSUPPORTED
 
 
@@ -113,3 +113,18 @@ def test_f64_deterministic_and_close_to_fp32_path():
     assert torch.equal(a, b)
     d = np.abs(R.wrap(a.cpu().numpy().astype(np.float64) - p.cpu().numpy()))
     assert np.sqrt(np.mean(d * d)) < 1e-5
+
+
+@pytest.mark.parametrize("fb", [False, True])
+@pytest.mark.parametrize("M,m", [(8, 3), (11, 6), (24, 12), (32, 20)])
+def test_f64_spatial_smoothing(M, m, fb):
+    """FP64 path with subarray order m (any m ≤ M; the FP32 kernel stops at 16)."""
+    H, W = (37, 45) if M < 19 else (M + 6, 75)
+    f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=3 * M + m), 5, snr_db=10.0)
+    v = bosrm.VARIANT_FP64 | (bosrm.VARIANT_FB if fb else 0)
+    out, fl, _, _ = bosrm.bos_rootmusic_demod_variant(f.to(DEV), M, variant=v, flags=True, subarray_len=m)
+    torch.cuda.synchronize()
+    g, gfl = out.cpu().numpy()[0], fl.cpu().numpy()[0]
+    o, ofl = R.demod_frame(f.numpy(), M, variant="fb" if fb else "paper", subarray_len=m)
+    assert_parity(g, o, ofl, f"FP64 SS M={M} m={m} fb={fb}", rms_tol=RMS64, max_tol=MAX64, max_excluded_frac=0.3)
+    assert flag_agreement(gfl, ofl) >= 0.995

@@ -108,10 +108,10 @@ def test_fb_nonfinite_and_errors():
     d = f.to(DEV)
     out = torch.empty(1, H, W, dtype=torch.float32, device=DEV)
     L = bosrm.lib()
-    rc = L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, 8, 3, 7, None, out.data_ptr(), None, None, None,
+    rc = L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, 8, 0, 3, 7, None, out.data_ptr(), None, None, None,
                                        torch.cuda.current_stream().cuda_stream)
     assert rc == bosrm.BOS_ERR_UNSUPPORTED
-    rc = L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, 8, 3, 1, None, None, None, None, None,
+    rc = L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, 8, 0, 3, 1, None, None, None, None, None,
                                        torch.cuda.current_stream().cuda_stream)
     assert rc == bosrm.BOS_ERR_INVALID_ARG
 
@@ -124,3 +124,86 @@ def test_fb_deterministic():
         torch.cuda.synchronize()
         assert torch.equal(a, b)
         del a, b
+
+
+# --------------------------------------------------------------------------------------
+# Spatial smoothing (subarray_len m < M), FP32 kernel demod_ss.cuh; m = 3 closed-form quartic
+# --------------------------------------------------------------------------------------
+def run_ss(frames_cpu, M, m, fb=False, ref=None, omega=False):
+    v = bosrm.VARIANT_FB if fb else bosrm.VARIANT_PAPER
+    r = None if ref is None else torch.as_tensor(ref, dtype=torch.float32).to(DEV)
+    out, fl, wx, wy = bosrm.bos_rootmusic_demod_variant(frames_cpu.to(DEV), M, variant=v, ref_phase=r, flags=True,
+                                                        omega=omega, subarray_len=m)
+    torch.cuda.synchronize()
+    shape = tuple(frames_cpu.shape)
+    res = [out.cpu().numpy().reshape(shape), fl.cpu().numpy().reshape(shape)]
+    if omega:
+        res += [wx.cpu().numpy().reshape(shape), wy.cpu().numpy().reshape(shape)]
+    return res
+
+
+@pytest.mark.parametrize("fb", [False, True])
+@pytest.mark.parametrize("M,m", [(4, 3), (5, 3), (8, 3), (8, 5), (11, 7), (16, 8), (17, 16), (24, 3), (24, 12),
+                                 (32, 16), (32, 3)])
+def test_ss_ragged_frame_parity(M, m, fb):
+    H, W = (37, 45) if M < 19 else (M + 6, 75)
+    f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M + m), 5, snr_db=10.0)
+    g, gfl = run_ss(f, M, m, fb)
+    o, ofl = R.demod_frame(f.numpy(), M, variant="fb" if fb else "paper", subarray_len=m)
+    assert_parity(g, o, ofl, f"SS ragged M={M} m={m} fb={fb}", max_excluded_frac=0.3)
+    assert np.all((gfl & bosrm.FLAG_BORDER) == (ofl & R.FLAG_BORDER))
+
+
+@pytest.mark.parametrize("M,m,snr", [(11, 6, 10.0), (8, 3, 0.0), (16, 3, 10.0), (16, 9, 20.0)])
+def test_ss_c2_sampled(M, m, snr):
+    w = synth.workload("C2")
+    stack = synth.make_stack(w, snr_db=snr)
+    d = stack.to(DEV)
+    ref = bosrm.bos_rootmusic_demod_variant(d[0:1], M, variant=0, subarray_len=m)[0]
+    out = bosrm.bos_rootmusic_demod_variant(d[1:2], M, variant=0, ref_phase=ref[0], subarray_len=m)[0]
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(int(snr) + 7 * M + m)
+    pix = (rng.integers(0, w.H, 8192), rng.integers(0, w.W, 8192))
+    o, ofl = R.demod_stack(stack.numpy(), M, pixels=pix, frame_indices=[1], subarray_len=m)
+    assert_parity(out[0].cpu().numpy()[pix], o[0], ofl[0], f"SS C2 M={M} m={m} snr={snr}")
+
+
+@pytest.mark.parametrize("M,m", [(8, 3), (9, 3), (8, 6)])
+def test_ss_noise_free_c1(M, m):
+    """Noise-free frames: the quartic / polynomial has a double root on the circle."""
+    w = synth.workload("C1")
+    f = synth.make_frame(w, 0)
+    g, gfl = run_ss(f, M, m)
+    o, ofl = R.demod_frame(f.numpy(), M, subarray_len=m)
+    assert_parity(g, o, ofl, f"SS C1 M={M} m={m}", max_excluded_frac=0.0)
+
+
+@pytest.mark.parametrize("M,m", [(8, 3), (12, 3), (20, 7)])
+def test_ss_plane_wave_and_omega(M, m):
+    H, W = 40, 70
+    wx, wy, a = -0.9, 0.55, 1.3
+    y, x = np.mgrid[0:H, 0:W]
+    f = torch.from_numpy(np.exp(1j * (wx * x + wy * y + a)).astype(np.complex64))
+    g, gfl, ox, oy = run_ss(f, M, m, omega=True)
+    ok = (gfl & (R.PARITY_EXCLUDE_MASK | R.FLAG_BORDER)) == 0
+    assert ok.mean() > 0.3
+    assert np.max(np.abs(ox - wx)[ok]) < 2e-3 and np.max(np.abs(oy - wy)[ok]) < 2e-3
+    assert np.max(np.abs(R.wrap(g - (wx * x + wy * y + a)))[ok]) < 2e-3
+
+
+def test_ss_argument_errors_and_nan():
+    H = W = 40
+    f = synth.make_frame(synth.workload("C1plane", H=H, W=W), 0).clone()
+    f[20, 20] = complex(float("nan"), 0.0)
+    g, gfl = run_ss(f, 9, 3)
+    o = R.window_offsets(9)
+    cover = (np.arange(H) >= 20 - o[-1]) & (np.arange(H) <= 20 - o[0])
+    assert np.array_equal(np.isnan(g), cover[:, None] & cover[None, :])
+    d = f.to(DEV)
+    out = torch.empty(1, H, W, dtype=torch.float32, device=DEV)
+    L = bosrm.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for m, rc in ((2, bosrm.BOS_ERR_INVALID_ARG), (9, bosrm.BOS_ERR_INVALID_ARG), (17, bosrm.BOS_ERR_UNSUPPORTED)):
+        M = 8 if m != 17 else 20
+        assert L.bos_rootmusic_demod_variant(d.data_ptr(), 1, H, W, M, m, 3, 0, None, out.data_ptr(), None, None, None,
+                                             s) == rc, (M, m)

@@ -33,8 +33,15 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--variant", default="paper", choices=["paper", "fb", "fp64", "fb_fp64"],
                     help="row f4 variants (timing + parity vs the oracle of the same variant; no iteration counts)")
+    ap.add_argument("--subarray", default="0",
+                    help="row f4 spatial smoothing order m: an int (0 = none) or 'half' (m = M // 2, ≥ 3)")
     args = ap.parse_args()
-    fb = args.variant != "paper"
+
+    def sub_of(M_):
+        if args.subarray == "half":
+            return max(3, M_ // 2)
+        return int(args.subarray)
+    fb = args.variant != "paper" or args.subarray != "0"
     vbits = {"paper": 0, "fb": bosrm.VARIANT_FB, "fp64": bosrm.VARIANT_FP64,
              "fb_fp64": bosrm.VARIANT_FB | bosrm.VARIANT_FP64}[args.variant]
     ovar = "fb" if args.variant.startswith("fb") else "paper"
@@ -42,7 +49,7 @@ def main():
     def demod(frames_, M_, ref_=None, out_=None):
         if fb:
             return bosrm.bos_rootmusic_demod_variant(frames_, M_, variant=vbits, ref_phase=ref_,
-                                                     out_phase=out_)[:2]
+                                                     out_phase=out_, subarray_len=sub_of(M_))[:2]
         return bosrm.bos_rootmusic_demod(frames_, M_, ref_phase=ref_, out_phase=out_)
 
     dev = torch.device("cuda", 0)
@@ -80,12 +87,13 @@ def main():
         rng = np.random.default_rng(M)
         pix = (rng.integers(0, w.H, 1024), rng.integers(0, w.W, 1024))
         host = frames[[0, T - 1]].cpu().numpy()
-        o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1], variant=ovar)
+        o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1], variant=ovar,
+                               subarray_len=(sub_of(M) or None) if fb else None)
         g = out[T - 1].cpu().numpy()[pix]
         valid = (ofl[0] & R.PARITY_EXCLUDE_MASK) == 0
         e = R.wrap(g - o[0])[valid]
         rms, mx = float(math.sqrt(np.mean(e * e))), float(np.max(np.abs(e)))
-        row = dict(M=M, variant=args.variant, mpix_s=mpx, fps_2048=mpx / (plane / 1e6), power_its=kpi, aberth_y=ky, aberth_x=kx,
+        row = dict(M=M, variant=args.variant, subarray=sub_of(M), mpix_s=mpx, fps_2048=mpx / (plane / 1e6), power_its=kpi, aberth_y=ky, aberth_x=kx,
                    kflop_px=fpx / 1e3, tflops=tf, frac=tf / peak, parity_rms=rms, parity_max=mx,
                    kernel="demod_kernel (thread/pixel)" if M <= 18 else "demod_wide_kernel (warp/pixel)")
         rows.append(row)
