@@ -281,7 +281,7 @@ def run_cuda(args, world, rank, local):
     except (OSError, ValueError, KeyError):
         traffic = None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/)", "kernel": f"bos::demod_kernel<{M},false>", "kernel_ms": kern_ms,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/)", "kernel": f"bos::{'demod_kernel' if M <= 18 else 'demod_wide_kernel'}<{M},false,false>", "kernel_ms": kern_ms,
                 "kernel_share_of_step": kern_ms / ms_per_step,
                 "flops_per_px": f_px, "iters": {"power": k_pi, "aberth_y": k_aby, "aberth_x": k_abx},
                 "peak_basis": f"FP32 FMA: {B200_SMS} SM x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",

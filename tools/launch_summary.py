@@ -28,7 +28,7 @@ n_other = 0
 for (i, n), m in k.items():
     t = m.get("gpu__time_duration.sum", 0.0)
     tot += t
-    if "bos::" in n:
+    if "bos::" in n or "demod" in n or "unwrap" in n or "lobe_mask" in n:
         dem += t
         print(f"| {i} | {n.split('(')[0]} | {t:.3f} | {m.get('dram__bytes_read.sum', float('nan')):.1f} | "
               f"{m.get('dram__bytes_write.sum', float('nan')):.1f} |")
