@@ -14,7 +14,7 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # BOS_LIBRARY overrides the library path (development A/B builds only)
-LIB_PATH = os.environ.get("BOS_LIBRARY", os.path.join(_PKG, "libbosrm.so"))
+LIB_PATH = os.environ.get("BOS_LIBRARY") or os.path.join(_PKG, "libbosrm.so")
 
 BOS_OK = 0
 BOS_ERR_INVALID_ARG = -1
