@@ -56,6 +56,16 @@ constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.0
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;
+// A first polish step already below this (|Δz| < 1e-4) ends the polish: Newton is quadratic,
+// so the root is then within ≈ C·|Δz|² of its FP32 value (C = |P″/2P′|, ~1–10 away from
+// double roots) — the second step would only confirm it.
+#ifndef BOS_POLISH_ONE_STEP2
+#define BOS_POLISH_ONE_STEP2 1e-8f
+#endif
+constexpr float kPolishOneStep2 = BOS_POLISH_ONE_STEP2;
+__device__ __forceinline__ bool polish_done(int t, float w2) {
+    return (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) || w2 < kPolishOneStep2;
+}
 constexpr float kRefineMargin = 0.05f; // selection margin (|ln|z||) below which the runner-up is polished too
 constexpr float kMoved2 = 1e-2f;       // polish displacement² (> 0.1) that triggers tight re-convergence
 constexpr float kAberthTightTol2 = 1e-10f;
@@ -666,7 +676,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             const float2 w = polish_step<N>(c, zs);
                             const float w2 = cabs2(w);
                             if (w2 < 1e30f) zs = csub(zs, w);
-                            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                            if (polish_done(t, w2)) break;
                         }
                         // Loose sweeps can park an approximation between roots; polished, it lands on
                         // a root that is no longer the closest (or moves far).  Then converge all
@@ -688,7 +698,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             const float2 w = polish_step<N>(c, z2);
                             const float w2 = cabs2(w);
                             if (w2 < 1e30f) z2 = csub(z2, w);
-                            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                            if (polish_done(t, w2)) break;
                         }
                         const float d1 = ln_dist(zs), d2 = ln_dist(z2);
                         if (d2 < d1) zs = z2;

@@ -162,7 +162,7 @@ __device__ __forceinline__ float2 ss_root(const float2 (&q)[MS], float& marg, bo
             const float2 w = polish_step<N>(c, zs);
             const float w2 = cabs2(w);
             if (w2 < 1e30f) zs = csub(zs, w);
-            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+            if (polish_done(t, w2)) break;
         }
     } else {
         cx2 z[N / 2];
@@ -180,7 +180,7 @@ __device__ __forceinline__ float2 ss_root(const float2 (&q)[MS], float& marg, bo
                 const float2 w = polish_step<N>(c, zs);
                 const float w2 = cabs2(w);
                 if (w2 < 1e30f) zs = csub(zs, w);
-                if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                if (polish_done(t, w2)) break;
             }
             const float dsel = ln_dist(zs), dsec = ln_dist(z2) - 1e-3f;
             if (attempt == 0 && (!(dsel <= dsec || marg == CUDART_INF_F) || !(cabs2(csub(zs, zsel)) <= kMoved2))) {
@@ -196,7 +196,7 @@ __device__ __forceinline__ float2 ss_root(const float2 (&q)[MS], float& marg, bo
             const float2 w = polish_step<N>(c, z2);
             const float w2 = cabs2(w);
             if (w2 < 1e30f) z2 = csub(z2, w);
-            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+            if (polish_done(t, w2)) break;
         }
         const float d1 = ln_dist(zs), d2 = ln_dist(z2);
         if (d2 < d1) zs = z2;

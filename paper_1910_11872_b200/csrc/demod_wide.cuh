@@ -471,7 +471,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             const float2 wp = newton_ratio_warp<N>(coef, zb, lane);
                             const float w2 = cabs2(wp);
                             if (w2 < 1e30f) zb = csub(zb, wp);
-                            if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                            if (polish_done(t, w2)) break;
                         }
                         const float dsel = ln_dist(zb), dsec = ln_dist(z2) - 1e-3f;   // see demod_kernel.cuh
                         if (attempt == 0 && (!(dsel <= dsec || !(second < CUDART_INF_F)) ||
@@ -487,7 +487,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                                 const float2 wp = newton_ratio_warp<N>(coef, z2, lane);
                                 const float w2 = cabs2(wp);
                                 if (w2 < 1e30f) z2 = csub(z2, wp);
-                                if (t + 1 >= kPolishMin && !(w2 > kPolishTol2)) break;
+                                if (polish_done(t, w2)) break;
                             }
                             const float d1 = ln_dist(zb), d2 = ln_dist(z2);
                             if (d2 < d1) zb = z2;

@@ -29,7 +29,7 @@ base = int(data[0][ix['Address']], 16)
 by_outer = collections.Counter(); by_inner = collections.Counter(); tot = 0
 for r in data:
     a = int(r[ix['Address']], 16) - base
-    ex = int(r[ix['Thread Instructions Executed']] or 0)
+    ex = int(r[ix[os.environ.get('COL', 'Thread Instructions Executed')]] or 0)
     tot += ex
     ch = addr2.get(a, ([], ''))[0]
     kl = [ln for f, ln in ch if f.endswith(os.path.basename(os.environ.get('SRC','demod_kernel.cuh')))]
