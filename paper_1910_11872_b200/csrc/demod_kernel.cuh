@@ -46,6 +46,21 @@ constexpr float kPowerTol = 1e-8f;    // ‖u_{k+1} − u_k‖² stop (error ≈
 // for.  Seen with the FB variant's polynomials (clamped border windows); always on there.
 // The paper path keeps the plain step test (−11 % throughput at 10 dB otherwise; DESIGN.md
 // §6 measures how often the two differ); BOS_STOP_NEWTON_PAPER=1 turns it on there too.
+#ifndef BOS_PREFETCH
+#define BOS_PREFETCH 1
+#endif
+#ifndef BOS_ITEMS_PER_CTA
+#define BOS_ITEMS_PER_CTA 4
+#endif
+constexpr int kItemsPerCta = BOS_ITEMS_PER_CTA;   // (frame, row block) work items per CTA
+template <int M>
+constexpr bool kPrefetch() { return BOS_PREFETCH != 0 && M <= 14; }   // 2 buffers ≤ 48 KB static SMEM
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 #ifndef BOS_STOP_NEWTON_PAPER
 #define BOS_STOP_NEWTON_PAPER 0
 #endif
@@ -482,33 +497,72 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
     // through frames independently (__syncwarp only), so a warp with slow pixels never holds
     // the other three at a CTA barrier.  Re-staging the M−1 overlap rows per warp costs ~10
     // LDG/STS per pixel of a ~7k-instruction pixel.
-    __shared__ float2 tiles[kBY][M * TW];
-    float2* tile = tiles[threadIdx.y];
+    __shared__ float2 tiles[kPrefetch<M>() ? 2 : 1][kBY][M * TW];
+    float2* tile = tiles[0][threadIdx.y];
 
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int x0 = blockIdx.x * kBX, y0 = blockIdx.y * kBY;
-    const int px = x0 + tx, py = y0 + ty;
+    const int x0 = blockIdx.x * kBX;
+    const int px = x0 + tx;
     const size_t plane = (size_t)H * (size_t)W;
-    if (py >= H) return;                         // warp-uniform: the whole row is outside
+    // work item = (frame, block of kBY rows); a CTA walks items blockIdx.y, +gridDim.y, … of its
+    // 32-column strip (several per CTA, so the next item's halo can be prefetched)
+    const int nby = (H + kBY - 1) / kBY;
+    const long long nitems = (long long)n_frames * nby;
+    // item → (frame, row block) advanced incrementally (no 64-bit division per item)
+    const int step_f = (int)(gridDim.y / (unsigned)nby), step_b = (int)(gridDim.y % (unsigned)nby);
+    auto advance = [&](int& fr, int& bl) {
+        fr += step_f;
+        bl += step_b;
+        if (bl >= nby) { bl -= nby; ++fr; }
+    };
 
-    for (int f = blockIdx.z; f < n_frames; f += gridDim.z) {
-        const float2* __restrict__ frame = frames + (size_t)f * plane;
-        // ---- a1: stage the clamped halo rows (Eq.(2) window support, [R1] clamp) ----
-        {
-            // row-wise: the clamped column offsets are per lane and frame-invariant, the row
-            // base is warp-uniform (no per-element division)
-            const int gx0 = min(max(x0 - O0 + tx, 0), W - 1);
-            const int gx1 = min(max(x0 - O0 + tx + kBX, 0), W - 1);
+    // a1: the clamped halo rows (Eq.(2) window support, [R1] clamp), row-wise: the clamped
+    // column offsets are per lane and invariant, the row base is warp-uniform.  With prefetch
+    // (kPrefetch) the next item's rows are copied by cp.async into the other buffer while this
+    // item's pixels are computed.
+    constexpr bool kPf = kPrefetch<M>();
+    const int gx0 = min(max(x0 - O0 + tx, 0), W - 1);
+    const int gx1 = min(max(x0 - O0 + tx + kBX, 0), W - 1);
+    auto stage_async = [&](int fr, int bl, float2* dst) {
+        const float2* __restrict__ fb = frames + (size_t)fr * plane;
+        const int pyr = bl * kBY + ty;
+#pragma unroll 2
+        for (int r = 0; r < M; ++r) {
+            const float2* __restrict__ row = fb + (size_t)min(max(pyr - O0 + r, 0), H - 1) * W;
+            cp_async8(dst + r * TW + tx, row + gx0);
+            if (tx + kBX < TW) cp_async8(dst + r * TW + tx + kBX, row + gx1);
+        }
+        cp_async_commit();
+    };
+    int buf = 0;
+    int f = (int)(blockIdx.y / (unsigned)nby), blk = (int)(blockIdx.y % (unsigned)nby);
+    if constexpr (kPf) {
+        if ((long long)blockIdx.y < nitems) stage_async(f, blk, tiles[0][ty]);
+    }
+    for (long long it = blockIdx.y; it < nitems; it += gridDim.y, advance(f, blk)) {
+        const int py = blk * kBY + ty;
+        if constexpr (kPf) {
+            cp_async_wait_all();
+            __syncwarp();
+            tile = tiles[buf][ty];
+            if (it + (long long)gridDim.y < nitems) {
+                int fn = f, bn = blk;
+                advance(fn, bn);
+                stage_async(fn, bn, tiles[buf ^ 1][ty]);
+            }
+            buf ^= 1;
+        } else {
+            const float2* __restrict__ frame = frames + (size_t)f * plane;
 #pragma unroll 2
             for (int r = 0; r < M; ++r) {
                 const float2* __restrict__ row = frame + (size_t)min(max(py - O0 + r, 0), H - 1) * W;
                 tile[r * TW + tx] = __ldg(row + gx0);
                 if (tx + kBX < TW) tile[r * TW + tx + kBX] = __ldg(row + gx1);
             }
+            __syncwarp();
         }
-        __syncwarp();
 
-        if (px < W) {
+        if (px < W && py < H) {             // warp-uniform in py
             const float2* win = tile + tx;             // Γ_w(i,k) = win[i*TW + k]
             uint8_t fl = 0;
             if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
