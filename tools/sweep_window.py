@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--frames", type=int, default=8)
     ap.add_argument("--size", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--parity-px", type=int, default=1024, help="sampled pixels of one frame checked vs the oracle")
     ap.add_argument("--variant", default="paper", choices=["paper", "fb", "fp64", "fb_fp64"],
                     help="row f4 variants (timing + parity vs the oracle of the same variant; no iteration counts)")
     ap.add_argument("--subarray", default="0",
@@ -85,7 +86,7 @@ def main():
             fpx = bench.flops_per_pixel(M, kpi, ky, kx)
         tf = fpx * mpx * 1e6 / 1e12
         rng = np.random.default_rng(M)
-        pix = (rng.integers(0, w.H, 1024), rng.integers(0, w.W, 1024))
+        pix = (rng.integers(0, w.H, args.parity_px), rng.integers(0, w.W, args.parity_px))
         host = frames[[0, T - 1]].cpu().numpy()
         o, ofl = R.demod_stack(host, M, pixels=pix, frame_indices=[1], variant=ovar,
                                subarray_len=(sub_of(M) or None) if fb else None)
