@@ -53,8 +53,11 @@ constexpr float kPowerTol = 1e-8f;    // ‖u_{k+1} − u_k‖² stop (error ≈
 #define BOS_ITEMS_PER_CTA 4
 #endif
 constexpr int kItemsPerCta = BOS_ITEMS_PER_CTA;   // (frame, row block) work items per CTA
+#ifndef BOS_PREFETCH_MAX_M
+#define BOS_PREFETCH_MAX_M 15   // M = 16: −9 % with prefetch (1 CTA/SM, 48 KB tiles), M = 15: +1.3 %
+#endif
 template <int M>
-constexpr bool kPrefetch() { return BOS_PREFETCH != 0 && M <= 14; }   // 2 buffers ≤ 48 KB static SMEM
+constexpr bool kPrefetch() { return BOS_PREFETCH != 0 && M <= BOS_PREFETCH_MAX_M; }   // 2 buffers ≤ 48 KB static SMEM (M ≤ 16)
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
