@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--window-len", type=int, default=8)
     p.add_argument("--ref-mode", default="recompute", choices=["recompute", "broadcast"])
     p.add_argument("--e2e-steps", type=int, default=None)
-    p.add_argument("--chunk-frames", type=int, default=10)
+    p.add_argument("--chunk-frames", type=int, default=5)   # e2e pipeline chunk: 4 → 2589, 5 → 2624, 10 → 2547, 20 → 2298 Mpixel/s
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-px", type=int, default=8192)
     p.add_argument("--cpu-sample-frames", type=int, default=8)
