@@ -11,6 +11,9 @@ flow frames r·(T−1)+1 … (r+1)·(T−1).  Two reference modes:
 * "broadcast": rank 0 demodulates the reference and NCCL-broadcasts φ_ref (4·H·W bytes)
   over NVLink; the others wait for it.  For streams whose reference frame lives on one
   rank only.
+
+``gather_results`` is the optional result gather of SURVEY §8(e): the ranks' flow-frame phase
+maps assembled on one rank in global frame order (not part of the timed step).
 """
 
 from __future__ import annotations
@@ -66,3 +69,20 @@ def sharded_stack_step(local_frames: torch.Tensor, demod, demod_raw, ref_mode: s
     else:
         raise ValueError(ref_mode)
     return demod(local_frames, ref), ref
+
+
+def gather_results(local_out: torch.Tensor, dst: int = 0):
+    """Assemble the job's output stack on rank ``dst``: [world·(T−1)+1, H, W] in global frame
+    order (frame 0 = the reference's own output, identical on every rank), None elsewhere.
+    local_out: this rank's [T, H, W] output (local frame 0 = the reference).  One collective
+    (all_gather of the flow frames: NCCL supports it on every build; gather is not universal)."""
+    if not is_dist() or dist.get_world_size() == 1:
+        return local_out
+    world, rank = dist.get_world_size(), dist.get_rank()
+    flows = local_out[1:].contiguous()
+    parts = [torch.empty_like(flows) for _ in range(world)]
+    dist.all_gather(parts, flows)
+    if rank != dst:
+        return None
+    return torch.cat([local_out[:1]] + parts, dim=0)
+

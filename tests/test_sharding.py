@@ -72,7 +72,8 @@ def _worker(rank, world, port, mode, T, H, W, M, q):
         ref_buf = torch.empty(H, W, dtype=torch.float32)
         out, ref = sharding.sharded_stack_step(frames, demod, demod_raw, mode, ref_buf)
         t = sharding.max_over_ranks(float(rank + 1))
-        q.put((rank, idx, out.numpy(), ref.numpy(), t))
+        g = sharding.gather_results(out)
+        q.put((rank, idx, out.numpy(), ref.numpy(), t, None if g is None else g.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -98,10 +99,14 @@ def test_two_rank_sharded_stack_matches_single_process(mode):
     g = synth.make_stack(w, frames=range(world * (T - 1) + 1))
     ref = demod_raw(g[0])
     full = demod(g, ref).numpy()
-    for rank, idx, out, rref, tmax in res:
+    for rank, idx, out, rref, tmax, gathered in res:
         assert tmax == float(world)                       # MAX over ranks
         assert np.array_equal(rref, ref.numpy())          # identical reference on every rank
         assert np.array_equal(out, full[idx])             # bitwise equal to the 1-process stack
+        if rank == 0:                                     # optional result gather (§8(e))
+            assert np.array_equal(gathered, full)
+        else:
+            assert gathered is None
 
 
 def test_bench_reference_arm_two_ranks_gloo():
