@@ -266,6 +266,32 @@ def test_64bit_offsets_stack_beyond_2p32_pixels():
     torch.cuda.empty_cache()
 
 
+def test_c5_full_stack_on_one_gpu():
+    """BASELINE config 5 at full size on ONE GPU (what 1 of the 1/2/4/8 shards would hold at
+    N = 1): 2048² × 2000 frames of the C5 generator (8.4e9 pixels, 62.5 GiB in, 31 GiB out), one
+    stack call at M = 8; sampled pixels of frames {1, 1000, 1999} against the oracle."""
+    free, _ = torch.cuda.mem_get_info()
+    w = synth.workload("C5")
+    T, H, W = w.T, w.H, w.W
+    need = T * H * W * (8 + 4) + (4 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB free")
+    frames = torch.empty(T, H, W, dtype=torch.complex64, device=DEV)
+    for t in range(T):
+        frames[t] = synth.make_frame(w, t, device=DEV)
+    out, _, ref = bosrm.bos_rootmusic_demod_stack(frames, 8, ref_index=0)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(55)
+    pix = (rng.integers(0, H, 4096), rng.integers(0, W, 4096))
+    picks = [1, 1000, T - 1]
+    host = frames[[0] + picks].cpu().numpy()
+    o, ofl = R.demod_stack(host, 8, ref_index=0, pixels=pix, frame_indices=[1, 2, 3])
+    for j, t in enumerate(picks):
+        assert_parity(out[t].cpu().numpy()[pix], o[j], ofl[j], f"C5 frame {t} of {T}")
+    del frames, out
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("M", [24, 32])
 def test_c4_large_windows_sampled_parity(M):
     """C4 frames (2048², diffusion flow, 10 dB) at large windows: 2048 random pixels of frame 7,
