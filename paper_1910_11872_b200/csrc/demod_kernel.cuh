@@ -70,7 +70,17 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <bool FB>
 constexpr bool newton_stop() { return FB || BOS_STOP_NEWTON_PAPER != 0; }
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
-constexpr float kAberthTol2 = 1e-3f;  // max_i |Δz_i|² sweep stop (|Δz| < 0.032), then polish
+// Loose sweep stop max_i |Δz_i|² < tol, then the Newton polish of the selected root.  The
+// thread kernel (Gauss–Seidel sweeps) uses 2e-3 (|Δz| < 0.045): a warp runs as many sweeps as
+// its slowest lane, and at 1e-3 the ~4 % of pixels needing a second sweep made most warps do
+// two (C3 M = 8: 2725 → 3263 Mpixel/s; 3e-3: 3290 but −7 % at 0 dB from more tight re-runs;
+// A/B vs 1e-3 over ~170 M pixels, 0–40 dB and noise-free: no pixel moved by > 1e-4 rad).
+// The warp kernel (Jacobi sweeps) keeps 1e-3: at 3e-3 it misplaced 7 of 17 M pixels.
+#ifndef BOS_ABERTH_TOL2
+#define BOS_ABERTH_TOL2 2e-3f
+#endif
+constexpr float kAberthTol2 = BOS_ABERTH_TOL2;  // thread kernel (demod_kernel, demod_ss)
+constexpr float kAberthTol2Wide = 1e-3f;       // warp kernel (demod_wide)
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;

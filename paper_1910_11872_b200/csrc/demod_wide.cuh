@@ -406,7 +406,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         cx2 zp = f2_cx2(z);
                         int it = 0;
                         bool ok = false;
-                        float tol2 = kAberthTol2;
+                        float tol2 = kAberthTol2Wide;
                         float2 zb, z2;
                         float marg;
                         int sl;

@@ -16,24 +16,37 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-CASES = [("C3", 8, 20), ("C3", 11, 20), ("C4", 16, 2), ("C4", 24, 2), ("C4", 32, 2)]
+# (workload, M, flow frames, SNR dB override or None = the workload's own)
+CASES = [("C3", 8, 20, None), ("C3", 11, 20, None), ("C4", 16, 2, None), ("C4", 24, 2, None), ("C4", 32, 2, None)]
+if os.environ.get("AB_SNR_SET"):
+    CASES = [("C3", 8, 10, 0.0), ("C3", 11, 10, 0.0), ("C3", 15, 4, 0.0), ("C3", 8, 10, 5.0), ("C3", 8, 10, 20.0),
+             ("C3", 8, 10, 40.0), ("C1", 8, 0, None), ("C1", 9, 0, None), ("C4", 12, 2, 0.0), ("C4", 16, 2, 5.0)]
 
 
-def stack_for(name, nframes):
+def stack_for(name, nframes, snr=None):
     from paper_1910_11872_b200 import synth
     w = synth.workload(name)
-    return synth.make_stack(w, frames=range(nframes + 1))
+    s = "default" if snr is None else snr
+    if nframes == 0:                                     # single-frame workloads: frame twice
+        f = synth.make_frame(w, 0, snr_db=s)
+        import torch
+        return torch.stack([f, f])
+    return synth.make_stack(w, frames=range(nframes + 1), snr_db=s)
+
+
+def key(name, M, snr):
+    return f"{name}_M{M}" + ("" if snr is None else f"_{snr:g}dB")
 
 
 def dump(path):
     import torch
     from paper_1910_11872_b200 import bosrm
     out = {}
-    for name, M, F in CASES:
-        st = stack_for(name, F).to("cuda")
+    for name, M, F, snr in CASES:
+        st = stack_for(name, F, snr).to("cuda")
         ph, _, _ = bosrm.bos_rootmusic_demod_stack(st, M, ref_index=0)
         torch.cuda.synchronize()
-        out[f"{name}_M{M}"] = ph[1:].cpu().numpy()
+        out[key(name, M, snr)] = ph[1:].cpu().numpy()
         del st, ph
     np.savez(path, **out)
 
@@ -41,13 +54,13 @@ def dump(path):
 def compare(pa, pb):
     from oracle import rootmusic as R
     a, b = np.load(pa), np.load(pb)
-    for name, M, F in CASES:
-        k = f"{name}_M{M}"
+    for name, M, F, snr in CASES:
+        k = key(name, M, snr)
         d = np.abs(R.wrap(a[k].astype(np.float64) - b[k]))
         bad = np.argwhere(np.nan_to_num(d, nan=10.0) > 1e-4)
         line = f"{k}: {d.size} px, {len(bad)} differ > 1e-4 rad"
         if len(bad):
-            st = stack_for(name, F).numpy()
+            st = stack_for(name, F, snr).numpy()
             ea, eb = [], []
             for t, y, x in bad[:40]:
                 o, _ = R.demod_stack(st[[0, t + 1]], M, pixels=(np.array([y]), np.array([x])), frame_indices=[1])
