@@ -39,7 +39,10 @@ constexpr int kBY = 4;                // rows per CTA
 constexpr int kThreads = kBX * kBY;
 
 constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyond)
-constexpr float kPowerTol = 1e-8f;    // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2) ≤ 3.3e-4 where σ1²/σ2² ≥ 1.3)
+#ifndef BOS_POWER_TOL
+#define BOS_POWER_TOL 1e-8f
+#endif
+constexpr float kPowerTol = BOS_POWER_TOL;    // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2) ≤ 3.3e-4 where σ1²/σ2² ≥ 1.3)
 // NEWTON_STOP sweeps also require every Newton ratio |P/P′|² < tol2, not only every Aberth
 // step: an approximation repelled by its neighbours can take small steps far from any root
 // (the repulsion term balances P/P′), and the loose stop then misses the root it is heading
