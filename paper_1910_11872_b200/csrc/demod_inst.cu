@@ -19,7 +19,7 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
     const dim3 block(kBX, kBY, 1);
-    if constexpr (M >= kWideMinM) {
+    if constexpr (M >= wide_min_m<FB>()) {
         const dim3 grid((unsigned)((W + kBX - 1) / kBX), (unsigned)((H + kBY - 1) / kBY),
                         (unsigned)std::min(n_frames, 65535));
         demod_wide_kernel<M, COUNT, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
@@ -33,7 +33,14 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
         const int ipc = (kPrefetch<M>() && nbx * items >= (long long)kItemsPerCta * 148 * 4 * 16) ? kItemsPerCta : 1;
         const long long gy = std::min<long long>((items + ipc - 1) / ipc, 65535);
         const dim3 grid((unsigned)nbx, (unsigned)gy, 1u);
-        demod_kernel<M, COUNT, FB><<<grid, block, 0, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
+        size_t dyn = 0;
+        if constexpr (kRsmem<M, FB>()) {                  // R_y triangles in dynamic shared memory
+            dyn = (size_t)kThreads * (M * (M - 1) / 2) * sizeof(unsigned long long);
+            const cudaError_t e = cudaFuncSetAttribute(demod_kernel<M, COUNT, FB>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            if (e != cudaSuccess) return e;
+        }
+        demod_kernel<M, COUNT, FB><<<grid, block, dyn, s>>>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters);
     }
     return cudaGetLastError();
 }

@@ -494,6 +494,107 @@ __device__ __forceinline__ int power_iteration_fb(const float (&Rd)[M], const cx
     return n;
 }
 
+// ---- R_y in shared memory for larger windows (kRsmem): from M = 15 the strict lower triangle
+// alone (M(M−1) registers) no longer fits beside the rest of the pixel's state and spilled to
+// local memory.  Each thread keeps its triangle in a per-thread slice of dynamic shared memory
+// (entry t at Rs[t·kThreads]: consecutive threads → consecutive words, conflict-free), built in
+// two register-blocked passes over row ranges and read once per power-iteration matvec.
+#ifndef BOS_RSMEM_MIN_M
+#define BOS_RSMEM_MIN_M 17
+#endif
+template <int M, bool FB>
+constexpr bool kRsmem() { return !FB && M >= BOS_RSMEM_MIN_M && M <= 20; }
+template <int M>
+constexpr int rsmem_split() {          // first row of the second pass: ≈ half the triangle's entries each
+    int r = 1, acc = 0;
+    while (r < M && 2 * (acc + r) <= M * (M - 1) / 2) acc += r++;
+    return r;
+}
+
+// Rows [LO, HI) of the strict lower triangle of R_y (entries R_ij, j < i) accumulated over the
+// M columns of the window in registers, then stored to the thread's shared-memory slice.
+template <int M, int TW, int LO, int HI>
+__device__ __forceinline__ void cov_pass_smem(const float2* win, cx2* Rs) {
+    constexpr int E = (HI * (HI - 1) - LO * (LO - 1)) / 2;
+    constexpr int B = LO * (LO - 1) / 2;               // tri_off(LO, 0)
+    cx2 acc[E > 0 ? E : 1];
+#pragma unroll
+    for (int t = 0; t < E; ++t) acc[t] = 0ull;
+    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+#pragma unroll 1
+    for (int k = 0; k < M; ++k) {
+        cx2 col[HI], colnj[HI];
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const float2 g = win[i * TW + k];
+            col[i] = cx2_make(g.x, g.y);
+            colnj[i] = mul2(cx2_make(g.y, g.x), kPosNeg);
+        }
+#pragma unroll
+        for (int i = LO; i < HI; ++i) {
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                cx2& r = acc[tri_off<M>(i, j) - B];
+                r = fma2(cx2_bcast(cx2_re(col[j])), col[i], fma2(cx2_bcast(cx2_im(col[j])), colnj[i], r));
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < E; ++t) Rs[(B + t) * kThreads] = acc[t];
+}
+
+// Power iteration as power_iteration() with R's strict lower triangle read from Rs.
+template <int M>
+__device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const cx2* Rs, cx2 (&u)[M], bool& ok) {
+    float2 r1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Rs[tri_off<M>(i + 1, i) * kThreads]));
+    float2 e = make_float2(1.0f, 0.0f);
+    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+    {
+        float2 t = make_float2(rsqrtf(float(M)), 0.0f);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            u[i] = cx2_make(t.x, t.y);
+            t = cmul(t, e);
+        }
+    }
+    ok = false;
+    int n = 0;
+    for (; n < kPowerMaxIt;) {
+        cx2 uj[M], y[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));   // j·u
+            y[j] = mul2(cx2_bcast(Rd[j]), u[j]);
+        }
+        // each stored R_ij (i > j) serves y_i += R_ij u_j and y_j += conj(R_ij) u_i
+#pragma unroll
+        for (int i = 1; i < M; ++i) {
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                const cx2 r = Rs[tri_off<M>(i, j) * kThreads];
+                y[i] = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], y[i]));
+                y[j] = fma2(cx2_bcast(cx2_re(r)), u[i], fma2(cx2_bcast(-cx2_im(r)), uj[i], y[j]));
+            }
+        }
+        float nrm2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+        float diff = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const cx2 yn = mul2(y[i], inv);
+            diff += cabs2(cx2_f2(sub2(yn, u[i])));
+            u[i] = yn;
+        }
+        ++n;
+        if (diff < kPowerTol) { ok = true; break; }
+    }
+    return n;
+}
+
 // CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).
 template <int M>
 constexpr int min_blocks_per_sm() {
@@ -515,6 +616,9 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
     // LDG/STS per pixel of a ~7k-instruction pixel.
     __shared__ float2 tiles[kPrefetch<M>() ? 2 : 1][kBY][M * TW];
     float2* tile = tiles[0][threadIdx.y];
+    constexpr bool kRs = kRsmem<M, FB>();
+    extern __shared__ cx2 rs_dyn[];                     // kRs: kThreads × NOFF (dynamic)
+    cx2* Rs = rs_dyn + threadIdx.y * kBX + threadIdx.x;
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int x0 = blockIdx.x * kBX;
@@ -587,12 +691,24 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
             // ---- a2: R_y = Γ_w Γ_w^H, diagonal (real) + strict lower triangle ----
             // R_ij += a·conj(b) (a = Γ(i,k), b = Γ(j,k)) = re(b)·a + im(b)·(−j·a): two FFMA2.
             float Rd[M];
-            cx2 Ro[NOFF > 0 ? NOFF : 1];
+            cx2 Ro[(NOFF > 0 && !kRs) ? NOFF : 1];
 #pragma unroll
             for (int i = 0; i < M; ++i) Rd[i] = 0.0f;
+            const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+            if constexpr (kRs) {
+#pragma unroll 1
+                for (int k = 0; k < M; ++k) {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        const float2 g = win[i * TW + k];
+                        Rd[i] = fmaf(g.x, g.x, fmaf(g.y, g.y, Rd[i]));
+                    }
+                }
+                cov_pass_smem<M, TW, 1, rsmem_split<M>()>(win, Rs);
+                cov_pass_smem<M, TW, rsmem_split<M>(), M>(win, Rs);
+            } else {
 #pragma unroll
             for (int t = 0; t < NOFF; ++t) Ro[t] = 0ull;
-            const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
 #pragma unroll 1
             for (int k = 0; k < M; ++k) {   // rolled: one column of Γ_w per trip (code size, regs)
                 cx2 col[M], colnj[M];
@@ -612,6 +728,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     }
                 }
             }
+            }
             float trace = 0.0f;
 #pragma unroll
             for (int i = 0; i < M; ++i) trace += Rd[i];
@@ -625,8 +742,12 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 cx2 u[M];
                 bool pow_ok = false;
                 float2 v[M];
+                if constexpr (kRs) {
+                    n_pow = power_iteration_smem<M>(Rd, Rs, u, pow_ok);
+                }
                 if constexpr (!FB) {
                     // ---- a3: dominant eigenvector of R_y by power iteration ----
+                    if constexpr (!kRs) {
                     // start: u_i = e^{jω̂ i}/√M with e^{jω̂} ∝ Σ_i R[i+1][i] (lag-1 correlation)
                     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
@@ -675,6 +796,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         }
                         ++n_pow;
                         if (diff < kPowerTol) { pow_ok = true; break; }
+                    }
                     }
                     // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
                     cx2 unj[M];

@@ -22,10 +22,15 @@
 
 namespace bos {
 
+// Smallest window handled warp-per-pixel.  The thread kernel keeps R_y in shared memory for
+// M = 17…20 (kRsmem) and beats this kernel there (M = 19: 200 vs 154, M = 20: 166 vs 147
+// Mpixel/s); the FB variant (registers only) switches at 19.
 #ifndef BOS_WIDE_MIN_M
-#define BOS_WIDE_MIN_M 19
+#define BOS_WIDE_MIN_M 21
 #endif
-constexpr int kWideMinM = BOS_WIDE_MIN_M;   // smallest window handled warp-per-pixel
+constexpr int kWideMinM = BOS_WIDE_MIN_M;
+template <bool FB>
+constexpr int wide_min_m() { return FB ? (BOS_WIDE_MIN_M < 19 ? BOS_WIDE_MIN_M : 19) : BOS_WIDE_MIN_M; }
 
 __device__ __forceinline__ cx2 shfl_cx2(cx2 v, int src) {
     return (cx2)__shfl_sync(0xffffffffu, (unsigned long long)v, src);

@@ -225,7 +225,7 @@ def test_high_snr_and_noise_free_parity(M, snr):
     assert_parity(g, o, ofl, f"high-SNR M={M} snr={snr}", max_excluded_frac=0.02)
 
 
-@pytest.mark.parametrize("M", [17, 25])
+@pytest.mark.parametrize("M", [17, 20, 21, 25])
 def test_wide_kernel_nonfinite_does_not_leak_along_the_segment(M):
     """A NaN sample poisons only the windows that contain it: the sliding R_y update of the
     warp-per-pixel kernel rebuilds R after a non-finite window."""

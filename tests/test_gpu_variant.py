@@ -1,7 +1,7 @@
 """GPU parity of row f4 (forward–backward averaged covariances, NOT in the paper; DESIGN.md
 [R13]): bos_rootmusic_demod_variant(variant=BOS_VARIANT_FB) vs the oracle's
 ``estimate_windows(..., variant="fb")`` on the same seeded complex64 bytes, both kernels
-(thread-per-pixel M ≤ 18, warp-per-pixel M ≥ 19), same tolerance as the paper path."""
+(thread-per-pixel M ≤ 18, warp-per-pixel M ≥ 19 for FB), same tolerance as the paper path."""
 
 import numpy as np
 import pytest

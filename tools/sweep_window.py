@@ -96,7 +96,7 @@ def main():
         rms, mx = float(math.sqrt(np.mean(e * e))), float(np.max(np.abs(e)))
         row = dict(M=M, variant=args.variant, subarray=sub_of(M), mpix_s=mpx, fps_2048=mpx / (plane / 1e6), power_its=kpi, aberth_y=ky, aberth_x=kx,
                    kflop_px=fpx / 1e3, tflops=tf, frac=tf / peak, parity_rms=rms, parity_max=mx,
-                   kernel="demod_kernel (thread/pixel)" if M <= 18 else "demod_wide_kernel (warp/pixel)")
+                   kernel="demod_kernel (thread/pixel)" if M <= 20 else "demod_wide_kernel (warp/pixel)")
         rows.append(row)
         print(f"| {M} | {mpx:.1f} | {row['fps_2048']:.1f} | {kpi:.2f} | {ky:.2f}/{kx:.2f} | {fpx / 1e3:.1f} | "
               f"{tf:.1f} | {tf / peak:.3f} | {rms:.1e} / {mx:.1e} |", flush=True)
