@@ -223,12 +223,35 @@ int bos_vertical_profile(const float* phase, int n_frames, int H, int W, float* 
  *               n_frames) bytes, caller-owned.
  *   stream      cudaStream_t.  The FFTs use cuFFT (library FFT, plans made and destroyed per
  *               call); the call returns after the work has completed (it synchronises
- *               `stream` before destroying its plans).
+ *               `stream` before destroying its plans).  Repeated calls should use the planned
+ *               form below: cuFFT plan creation costs milliseconds to hundreds of ms of host time.
  */
 size_t bos_analytic_signal_workspace_bytes(int H, int W, int n_frames);
 int bos_analytic_signal(const uint8_t* frames_u8, int n_frames, int H, int W,
                         double fx, double fy, double radius, int remove_carrier,
                         bos_cf32* out, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Planned form of bos_analytic_signal: a caller-owned plan holds the cuFFT plans for H×W
+ * frames (a batch of min(max_frames, 8) frames and a single frame for ragged tails), so
+ * repeated calls make no plans and do not synchronise (stream-ordered, asynchronous).
+ *   bos_analytic_plan_create  H, W ≥ 2, max_frames ≥ 1; *plan receives the handle;
+ *                             *workspace_bytes (if not NULL) the cuFFT work-area size the
+ *                             planned calls need.  BOS_ERR_CUDA if cuFFT fails.
+ *   bos_analytic_signal_planned  as bos_analytic_signal with H, W taken from the plan; any
+ *                             n_frames ≥ 1.  A plan must not be used by two calls at once
+ *                             (it binds the work area and stream per call).
+ *   bos_analytic_plan_destroy releases the plan (NULL is a no-op); the caller first makes
+ *                             sure no planned call on it is still executing.
+ */
+typedef struct bos_analytic_plan bos_analytic_plan;
+int bos_analytic_plan_create(int H, int W, int max_frames, bos_analytic_plan** plan,
+                             size_t* workspace_bytes);
+int bos_analytic_signal_planned(bos_analytic_plan* plan, const uint8_t* frames_u8, int n_frames,
+                                double fx, double fy, double radius, int remove_carrier,
+                                bos_cf32* out, void* d_workspace, size_t workspace_bytes,
+                                void* stream);
+int bos_analytic_plan_destroy(bos_analytic_plan* plan);
 
 /*
  * bos_unwrap — SURVEY §8 row f2, the step after the path: 2-D phase unwrapping "followed by

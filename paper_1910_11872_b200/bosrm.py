@@ -51,6 +51,10 @@ SIGNATURES = {
     "bos_unwrap": (_I, [_VP, _I, _I, _I, _VP, _VP, _SZ, _VP]),
     "bos_analytic_signal": (_I, [_VP, _I, _I, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double, _I, _VP, _VP,
                                  _SZ, _VP]),
+    "bos_analytic_plan_create": (_I, [_I, _I, _I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_size_t)]),
+    "bos_analytic_signal_planned": (_I, [_VP, _VP, _I, ctypes.c_double, ctypes.c_double, ctypes.c_double, _I, _VP,
+                                         _VP, _SZ, _VP]),
+    "bos_analytic_plan_destroy": (_I, [_VP]),
     "bos_index_gradient": (_I, [_VP, _SZ, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                 _VP, _VP]),
     "bos_vertical_profile": (_I, [_VP, _I, _I, _I, _VP, _VP]),
@@ -318,6 +322,49 @@ def bos_analytic_signal(frames_u8: torch.Tensor, fx: float, fy: float, radius: f
                                    int(bool(remove_carrier)), out.data_ptr(), workspace.data_ptr(),
                                    workspace.numel(), _stream_ptr(stream))
     _check(rc, "bos_analytic_signal")
+    return out
+
+
+class AnalyticPlan:
+    """Caller-owned cuFFT plans for row f1 (bos_analytic_plan_create / _destroy): repeated
+    bos_analytic_signal_planned calls on H×W frames make no plans and do not synchronise."""
+
+    def __init__(self, H: int, W: int, max_frames: int, device=None):
+        self._h = ctypes.c_void_p()
+        ws = ctypes.c_size_t()
+        _check(lib().bos_analytic_plan_create(int(H), int(W), int(max_frames), ctypes.byref(self._h),
+                                              ctypes.byref(ws)), "bos_analytic_plan_create")
+        self.H, self.W = int(H), int(W)
+        self.workspace = torch.empty(max(int(ws.value), 256), dtype=torch.uint8,
+                                     device=device if device is not None else "cuda")
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().bos_analytic_plan_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:       # interpreter shutdown
+            pass
+
+
+def bos_analytic_signal_planned(plan: AnalyticPlan, frames_u8: torch.Tensor, fx: float, fy: float, radius: float,
+                                remove_carrier: bool = False, out: torch.Tensor | None = None,
+                                stream=None) -> torch.Tensor:
+    """Row f1 with a plan (AnalyticPlan): uint8 CUDA [T,H,W] → Γ complex64 [T,H,W], asynchronous."""
+    frames_u8 = _dev_tensor(_frames3(frames_u8), torch.uint8, "frames_u8")
+    T, H, W = frames_u8.shape
+    if (H, W) != (plan.H, plan.W):
+        raise ValueError(f"plan is for {plan.H}x{plan.W} frames, got {H}x{W}")
+    if out is None:
+        out = torch.empty(T, H, W, dtype=torch.complex64, device=frames_u8.device)
+    _dev_tensor(out, torch.complex64, "out")
+    rc = lib().bos_analytic_signal_planned(plan._h, frames_u8.data_ptr(), T, float(fx), float(fy), float(radius),
+                                           int(bool(remove_carrier)), out.data_ptr(), plan.workspace.data_ptr(),
+                                           plan.workspace.numel(), _stream_ptr(stream))
+    _check(rc, "bos_analytic_signal_planned")
     return out
 
 

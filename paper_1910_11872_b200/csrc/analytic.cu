@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <new>
 
 #include "bos_rootmusic.h"
 
@@ -101,15 +102,99 @@ unsigned grid_for(size_t n) { return (unsigned)std::min<size_t>((n + 255) / 256,
 
 }  // namespace
 
+// Caller-owned plan object (opaque in the ABI): the cuFFT plans for a chunk of kChunk frames
+// and for single frames (ragged tails), made once instead of per call.
+struct bos_analytic_plan {
+    int H, W, batch;
+    cufftHandle full, one;
+    size_t work;
+};
+
+namespace {
+
+int run_planned(bos_analytic_plan* pl, const uint8_t* frames_u8, int n_frames, double fx, double fy, double radius,
+                int remove, bos_cf32* out, void* d_workspace, size_t workspace_bytes, cudaStream_t s) {
+    const int H = pl->H, W = pl->W;
+    if (frames_u8 == nullptr || out == nullptr || d_workspace == nullptr) return BOS_ERR_INVALID_ARG;
+    if (n_frames < 1 || !(radius > 0.0)) return BOS_ERR_INVALID_ARG;
+    if (!(fx >= -0.5 && fx <= 0.5 && fy >= -0.5 && fy <= 0.5)) return BOS_ERR_INVALID_ARG;
+    if (fx * fx + fy * fy <= radius * radius) return BOS_ERR_INVALID_ARG;   // the disc must exclude DC
+    if (workspace_bytes < pl->work) return BOS_ERR_INVALID_ARG;
+    if (!is_dev(frames_u8) || !is_dev(out) || !is_dev(d_workspace)) return BOS_ERR_INVALID_ARG;
+    const size_t plane = (size_t)H * (size_t)W;
+    const uintptr_t a = (uintptr_t)frames_u8, b = (uintptr_t)out;
+    if (a < b + plane * (size_t)n_frames * sizeof(bos_cf32) && b < a + plane * (size_t)n_frames)
+        return BOS_ERR_INVALID_ARG;
+    for (cufftHandle h : {pl->full, pl->one})
+        if (cufftSetWorkArea(h, d_workspace) != CUFFT_SUCCESS || cufftSetStream(h, s) != CUFFT_SUCCESS)
+            return BOS_ERR_CUDA;
+    for (int f0 = 0; f0 < n_frames;) {
+        const int nb = (n_frames - f0 >= pl->batch) ? pl->batch : 1;     // ragged tail: frame by frame
+        const cufftHandle p = (nb == pl->batch) ? pl->full : pl->one;
+        float2* g = reinterpret_cast<float2*>(out) + (size_t)f0 * plane;
+        const size_t n = plane * (size_t)nb;
+        u8_to_complex<<<grid_for(n), 256, 0, s>>>(frames_u8 + (size_t)f0 * plane, n, g);
+        if (cufftExecC2C(p, (cufftComplex*)g, (cufftComplex*)g, CUFFT_FORWARD) != CUFFT_SUCCESS) return BOS_ERR_CUDA;
+        lobe_mask<<<grid_for(n), 256, 0, s>>>(g, nb, H, W, fx, fy, radius * radius);
+        if (cufftExecC2C(p, (cufftComplex*)g, (cufftComplex*)g, CUFFT_INVERSE) != CUFFT_SUCCESS) return BOS_ERR_CUDA;
+        if (remove) remove_carrier<<<grid_for(n), 256, 0, s>>>(g, nb, H, W, fx, fy);
+        if (cudaGetLastError() != cudaSuccess) return BOS_ERR_CUDA;
+        f0 += nb;
+    }
+    return BOS_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
+int bos_analytic_plan_create(int H, int W, int max_frames, bos_analytic_plan** plan, size_t* workspace_bytes) {
+    if (plan == nullptr || H < 2 || W < 2 || max_frames < 1) return BOS_ERR_INVALID_ARG;
+    *plan = nullptr;
+    bos_analytic_plan* pl = new (std::nothrow) bos_analytic_plan;
+    if (pl == nullptr) return BOS_ERR_CUDA;
+    pl->H = H;
+    pl->W = W;
+    pl->batch = std::min(max_frames, kChunk);
+    size_t w1 = 0, w2 = 0;
+    if (make_plan(&pl->full, H, W, pl->batch, &w1) != BOS_OK) {
+        delete pl;
+        return BOS_ERR_CUDA;
+    }
+    if (make_plan(&pl->one, H, W, 1, &w2) != BOS_OK) {
+        cufftDestroy(pl->full);
+        delete pl;
+        return BOS_ERR_CUDA;
+    }
+    pl->work = std::max<size_t>(std::max(w1, w2), 256);
+    if (workspace_bytes != nullptr) *workspace_bytes = pl->work;
+    *plan = pl;
+    return BOS_OK;
+}
+
+int bos_analytic_plan_destroy(bos_analytic_plan* plan) {
+    if (plan == nullptr) return BOS_OK;
+    cufftDestroy(plan->full);
+    cufftDestroy(plan->one);
+    delete plan;
+    return BOS_OK;
+}
+
+int bos_analytic_signal_planned(bos_analytic_plan* plan, const uint8_t* frames_u8, int n_frames, double fx,
+                                double fy, double radius, int remove_carrier, bos_cf32* out, void* d_workspace,
+                                size_t workspace_bytes, void* stream) {
+    if (plan == nullptr) return BOS_ERR_INVALID_ARG;
+    return run_planned(plan, frames_u8, n_frames, fx, fy, radius, remove_carrier, out, d_workspace, workspace_bytes,
+                       static_cast<cudaStream_t>(stream));
+}
+
 size_t bos_analytic_signal_workspace_bytes(int H, int W, int n_frames) {
-    if (H < 1 || W < 1 || n_frames < 1) return 0;
-    cufftHandle plan;
+    if (H < 2 || W < 2 || n_frames < 1) return 0;
+    bos_analytic_plan* pl = nullptr;
     size_t work = 0;
-    if (make_plan(&plan, H, W, std::min(n_frames, kChunk), &work) != BOS_OK) return 0;
-    cufftDestroy(plan);
-    return work > 0 ? work : 256;
+    if (bos_analytic_plan_create(H, W, n_frames, &pl, &work) != BOS_OK) return 0;
+    bos_analytic_plan_destroy(pl);
+    return work;
 }
 
 int bos_analytic_signal(const uint8_t* frames_u8, int n_frames, int H, int W, double fx, double fy,
@@ -120,48 +205,13 @@ int bos_analytic_signal(const uint8_t* frames_u8, int n_frames, int H, int W, do
     if (!(fx >= -0.5 && fx <= 0.5 && fy >= -0.5 && fy <= 0.5)) return BOS_ERR_INVALID_ARG;
     if (fx * fx + fy * fy <= radius * radius) return BOS_ERR_INVALID_ARG;   // the disc must exclude DC
     if (!is_dev(frames_u8) || !is_dev(out) || !is_dev(d_workspace)) return BOS_ERR_INVALID_ARG;
-    const size_t plane = (size_t)H * (size_t)W;
-    const uintptr_t a = (uintptr_t)frames_u8, b = (uintptr_t)out;
-    if (a < b + plane * (size_t)n_frames * sizeof(bos_cf32) && b < a + plane * (size_t)n_frames)
-        return BOS_ERR_INVALID_ARG;
+    bos_analytic_plan* pl = nullptr;
+    if (bos_analytic_plan_create(H, W, n_frames, &pl, nullptr) != BOS_OK) return BOS_ERR_CUDA;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cufftHandle plan;
-    size_t work = 0;
-    const int batch = std::min(n_frames, kChunk);
-    if (make_plan(&plan, H, W, batch, &work) != BOS_OK) return BOS_ERR_CUDA;
-    int rc = BOS_OK;
-    if (workspace_bytes < work) rc = BOS_ERR_INVALID_ARG;
-    if (rc == BOS_OK && (cufftSetWorkArea(plan, d_workspace) != CUFFT_SUCCESS || cufftSetStream(plan, s) != CUFFT_SUCCESS))
-        rc = BOS_ERR_CUDA;
-    cufftHandle tail = 0;
-    bool have_tail = false;
-    for (int f0 = 0; rc == BOS_OK && f0 < n_frames; f0 += batch) {
-        const int nb = std::min(batch, n_frames - f0);
-        cufftHandle p = plan;
-        if (nb != batch) {                       // last partial chunk
-            size_t w2 = 0;
-            if (make_plan(&tail, H, W, nb, &w2) != BOS_OK || w2 > workspace_bytes ||
-                cufftSetWorkArea(tail, d_workspace) != CUFFT_SUCCESS || cufftSetStream(tail, s) != CUFFT_SUCCESS) {
-                rc = BOS_ERR_CUDA;
-                break;
-            }
-            have_tail = true;
-            p = tail;
-        }
-        float2* g = reinterpret_cast<float2*>(out) + (size_t)f0 * plane;
-        const size_t n = plane * (size_t)nb;
-        u8_to_complex<<<grid_for(n), 256, 0, s>>>(frames_u8 + (size_t)f0 * plane, n, g);
-        if (cufftExecC2C(p, (cufftComplex*)g, (cufftComplex*)g, CUFFT_FORWARD) != CUFFT_SUCCESS) rc = BOS_ERR_CUDA;
-        lobe_mask<<<grid_for(n), 256, 0, s>>>(g, nb, H, W, fx, fy, radius * radius);
-        if (rc == BOS_OK && cufftExecC2C(p, (cufftComplex*)g, (cufftComplex*)g, CUFFT_INVERSE) != CUFFT_SUCCESS)
-            rc = BOS_ERR_CUDA;
-        if (remove) remove_carrier<<<grid_for(n), 256, 0, s>>>(g, nb, H, W, fx, fy);
-        if (cudaGetLastError() != cudaSuccess) rc = BOS_ERR_CUDA;
-    }
+    int rc = run_planned(pl, frames_u8, n_frames, fx, fy, radius, remove, out, d_workspace, workspace_bytes, s);
     // cuFFT plans own device resources (twiddles): finish the queued work before destroying them
-    if (cudaStreamSynchronize(s) != cudaSuccess) rc = BOS_ERR_CUDA;
-    if (have_tail) cufftDestroy(tail);
-    cufftDestroy(plan);
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == BOS_OK) rc = BOS_ERR_CUDA;
+    bos_analytic_plan_destroy(pl);
     return rc;
 }
 

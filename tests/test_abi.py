@@ -134,6 +134,17 @@ def test_analytic_signal_argument_errors(L):
     assert f(p, 1, 16, 16, 0.2, 0.0, 0.0, 0, p + 1024, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
 
 
+def test_analytic_plan_argument_errors(L):
+    h = ctypes.c_void_p()
+    assert L.bos_analytic_plan_create(1, 16, 4, ctypes.byref(h), None) == bosrm.BOS_ERR_INVALID_ARG
+    assert L.bos_analytic_plan_create(16, 16, 0, ctypes.byref(h), None) == bosrm.BOS_ERR_INVALID_ARG
+    assert L.bos_analytic_plan_create(16, 16, 4, None, None) == bosrm.BOS_ERR_INVALID_ARG
+    buf = ctypes.create_string_buffer(64)
+    p = ctypes.addressof(buf)
+    assert L.bos_analytic_signal_planned(None, p, 1, 0.125, 0.0, 0.05, 0, p, p, 16, None) == bosrm.BOS_ERR_INVALID_ARG
+    assert L.bos_analytic_plan_destroy(None) == bosrm.BOS_OK
+
+
 def test_unwrap_workspace_and_errors(L):
     n = 100 * 64
     al = lambda v: (v + 255) // 256 * 256  # noqa: E731

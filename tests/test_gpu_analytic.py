@@ -39,6 +39,29 @@ def test_analytic_signal_matches_oracle(shape, remove):
     assert err.max() <= 2e-5 * np.abs(o).max(), (err.max(), np.abs(o).max())
 
 
+def test_planned_analytic_signal_matches_oracle_and_unplanned():
+    """The caller-owned plan (bos_analytic_plan_*) on a ragged frame count (2 full 8-frame
+    batches + 3 single-frame tail FFTs) equals the per-call-plan path bit for bit and the
+    oracle within the FP32 FFT bound; one plan serves calls of different frame counts."""
+    T, H, W = 19, 64, 80
+    w = synth.workload("C2", H=H, W=W, snr_db=10.0)
+    fr = torch.stack([synth.make_intensity_frame(w, t) for t in range(T)]).to(DEV)
+    plan = bosrm.AnalyticPlan(H, W, T)
+    for n in (T, 5, 1):
+        g = bosrm.bos_analytic_signal_planned(plan, fr[:n], synth.CARRIER_FX, synth.CARRIER_FY, 0.05, True)
+        u = bosrm.bos_analytic_signal(fr[:n], synth.CARRIER_FX, synth.CARRIER_FY, 0.05, True)
+        torch.cuda.synchronize()
+        assert torch.equal(g, u)
+    o = A.analytic_signal(fr.cpu().numpy(), synth.CARRIER_FX, synth.CARRIER_FY, 0.05, True)
+    g = bosrm.bos_analytic_signal_planned(plan, fr, synth.CARRIER_FX, synth.CARRIER_FY, 0.05, True)
+    torch.cuda.synchronize()
+    err = np.abs(g.cpu().numpy().astype(np.complex128) - o)
+    assert err.max() <= 2e-5 * np.abs(o).max()
+    with pytest.raises(ValueError):
+        bosrm.bos_analytic_signal_planned(plan, fr[:, :32], synth.CARRIER_FX, synth.CARRIER_FY, 0.05)
+    plan.close()
+
+
 def test_camera_to_phase_pipeline_parity():
     """8-bit C2 pair (reference + flow, 10 dB) → f1 → root-MUSIC stack demod (M = 11) on the
     GPU vs oracle f1 → oracle demod: sampled pixels within the north_star tolerance."""

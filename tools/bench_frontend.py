@@ -34,8 +34,10 @@ def main():
     out = torch.empty(T, w.H, w.W, dtype=torch.float32, device=dev)
     ref = torch.empty(w.H, w.W, dtype=torch.float32, device=dev)
 
+    plan = bosrm.AnalyticPlan(w.H, w.W, T)          # caller-owned cuFFT plans (no per-call plan/sync)
+
     def f1():
-        bosrm.bos_analytic_signal(u8, synth.CARRIER_FX, synth.CARRIER_FY, 0.05, False, out=gamma, workspace=ws)
+        bosrm.bos_analytic_signal_planned(plan, u8, synth.CARRIER_FX, synth.CARRIER_FY, 0.05, False, out=gamma)
 
     def pipe():
         f1()
@@ -51,9 +53,19 @@ def main():
         pipe()
         unwrap()
 
+    grad = torch.empty_like(out)
+    prof = torch.empty(T, w.H, dtype=torch.float32, device=dev)
+
+    def index_gradient():                     # row f3: Eq.(17) scale, 4 B in + 4 B out per pixel
+        bosrm.bos_index_gradient(unw, 1.333, 1.0, 1e4, 0.01, out=grad)
+
+    def vertical_profile():                   # row f3: column means, 4 B in per pixel
+        bosrm.bos_vertical_profile(grad, out=prof)
+
     res = {}
     for name, fn in (("analytic_signal", f1), ("pipeline_f1_plus_demod", pipe), ("unwrap", unwrap),
-                     ("pipeline_f1_demod_unwrap", full)):
+                     ("pipeline_f1_demod_unwrap", full), ("index_gradient", index_gradient),
+                     ("vertical_profile", vertical_profile)):
         for _ in range(3):                  # warm-up (lazy module loading, cuFFT plan creation paths)
             fn()
         torch.cuda.synchronize()
@@ -70,6 +82,16 @@ def main():
     # f1 DRAM traffic lower bound: 1 B in + 8 B out + 2 in-place FFTs (≥16 B r+w each) + mask (16 B) per pixel
     bytes_px = 1 + 8 + 2 * 16 + 16
     res["analytic_signal"]["achieved_gbs_lower_bound"] = bytes_px * T * plane / (res["analytic_signal"]["ms"] / 1e3) / 1e9
+    peak = 6533.8                             # MEASURED_PEAKS.json HBM copy GB/s (fallback if absent)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+        peak = float(next(v for k, v in peaks.items() if "hbm" in k.lower() and isinstance(v, (int, float))))
+    except (OSError, ValueError, StopIteration):
+        pass
+    for name, bpx in (("index_gradient", 8), ("vertical_profile", 4)):
+        gbs = bpx * T * plane / (res[name]["ms"] / 1e3) / 1e9
+        res[name].update(achieved_gbs=gbs, hbm_peak_gbs=peak, frac=gbs / peak)
     print(json.dumps({"workload": f"{w.H}x{w.W} x {T} 8-bit C3 intensity frames, carrier (1/16, 1/8), r = 0.05",
                       "window_len": args.window_len, **res}))
 
