@@ -157,16 +157,58 @@ __global__ void jump(size_t n, const int* __restrict__ parent, const int* __rest
     }
 }
 
-__global__ void anchor_max(size_t plane, int F, const double* __restrict__ rel, unsigned long long* best) {
-    const size_t n = plane * F;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        atomicMax(best + i / plane, (unsigned long long)__double_as_longlong(rel[i]));
+// Per-frame max reliability (step 4's anchor) and the lowest pixel index attaining it: grid.y
+// = frame, grid.x blocks stride over the plane; block-level reduction, then ONE atomic per
+// block (a per-pixel atomic on one address per frame serialised: 50 ms for 100 1024² frames).
+// Reliabilities are ≥ 0, so their IEEE bit patterns order like the values.
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
 }
-__global__ void anchor_argmin(size_t plane, int F, const double* __restrict__ rel, const unsigned long long* best,
+__device__ __forceinline__ unsigned warp_min_u32(unsigned v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__global__ void anchor_max(size_t plane, int f0, const double* __restrict__ rel, unsigned long long* best) {
+    __shared__ unsigned long long red[32];
+    const int f = f0 + (int)blockIdx.y;
+    const double* r = rel + (size_t)f * plane;
+    unsigned long long m = 0ull;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < plane; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long v = (unsigned long long)__double_as_longlong(r[i]);
+        m = v > m ? v : m;
+    }
+    m = warp_max_u64(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0ull;
+        m = warp_max_u64(m);
+        if (threadIdx.x == 0) atomicMax(best + f, m);
+    }
+}
+__global__ void anchor_argmin(size_t plane, int f0, const double* __restrict__ rel, const unsigned long long* best,
                               unsigned* idx) {
-    const size_t n = plane * F;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        if ((unsigned long long)__double_as_longlong(rel[i]) == best[i / plane]) atomicMin(idx + i / plane, (unsigned)i);
+    __shared__ unsigned red[32];
+    const int f = f0 + (int)blockIdx.y;
+    const double* r = rel + (size_t)f * plane;
+    const unsigned long long b = best[f];
+    unsigned m = 0xffffffffu;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < plane; i += (size_t)gridDim.x * blockDim.x)
+        if ((unsigned long long)__double_as_longlong(r[i]) == b) m = min(m, (unsigned)((size_t)f * plane + i));
+    m = warp_min_u32(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0xffffffffu;
+        m = warp_min_u32(m);
+        if (threadIdx.x == 0 && m != 0xffffffffu) atomicMin(idx + f, m);
+    }
 }
 
 __global__ void finish(size_t plane, int F, const float* __restrict__ w, const int* __restrict__ off,
@@ -296,8 +338,11 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
         if (cudaMemsetAsync(ws.amax, 0, nf * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(ws.aidx, 0xff, nf * sizeof(unsigned), s) != cudaSuccess)
             return BOS_ERR_CUDA;
-        anchor_max<<<gn, 256, 0, s>>>(plane, nf, ws.rel, ws.amax);
-        anchor_argmin<<<gn, 256, 0, s>>>(plane, nf, ws.rel, ws.amax, ws.aidx);
+        for (int a0 = 0; a0 < nf; a0 += 65535) {                  // grid.y = frames (≤ 65535 per launch)
+            const dim3 ga((unsigned)std::min<size_t>((plane + 255) / 256, 64), (unsigned)std::min(nf - a0, 65535));
+            anchor_max<<<ga, 256, 0, s>>>(plane, a0, ws.rel, ws.amax);
+            anchor_argmin<<<ga, 256, 0, s>>>(plane, a0, ws.rel, ws.amax, ws.aidx);
+        }
         finish<<<gn, 256, 0, s>>>(plane, nf, w, ws.off, ws.aidx, out);
         if (cudaGetLastError() != cudaSuccess) return BOS_ERR_CUDA;
     }
