@@ -52,18 +52,18 @@ __global__ void reliability_kernel(const float* __restrict__ w, int H, int W, in
     }
 }
 
-__global__ void init_kernel(size_t n, int* parent, int* off) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        parent[i] = (int)i;
-        off[i] = 0;
-    }
+// union-find node: parent (low 32 bits) and the 2π multiple relative to it (high 32 bits) in
+// ONE 64-bit word, so a concurrent reader always sees a consistent (parent, offset) pair and
+// pointer jumping can run in place
+__device__ __forceinline__ unsigned long long pk(int parent, int off) {
+    return (unsigned long long)(unsigned)parent | ((unsigned long long)(unsigned)off << 32);
 }
+__device__ __forceinline__ int par(unsigned long long w) { return (int)(unsigned)(w & 0xffffffffull); }
+__device__ __forceinline__ int ofs(unsigned long long w) { return (int)(unsigned)(w >> 32); }
 
-__global__ void reset_best(size_t n, unsigned long long* best_rel, unsigned* best_id) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        best_rel[i] = 0ull;
-        best_id[i] = 0xffffffffu;
-    }
+__global__ void init_kernel(size_t n, unsigned long long* po) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        po[i] = pk((int)i, 0);
 }
 
 // edge id e = 2p (p → p+1) or 2p+1 (p → p+W), p = frame·H·W + y·W + x (a batch of frames is one
@@ -83,13 +83,13 @@ __device__ __forceinline__ bool edge_ends(unsigned e, int H, int W, int& p, int&
 }
 
 // pass 1: every component's largest incident cross-edge reliability (positive doubles order as u64)
-__global__ void edge_max(int H, int W, int F, const double* __restrict__ rel, const int* __restrict__ parent,
-                         unsigned long long* best_rel) {
+__global__ void edge_max(int H, int W, int F, const double* __restrict__ rel,
+                         const unsigned long long* __restrict__ po, unsigned long long* best_rel) {
     const size_t ne = 2 * (size_t)H * W * F;
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x) {
         int p, q;
         if (!edge_ends((unsigned)e, H, W, p, q)) continue;
-        const int rp = parent[p], rq = parent[q];
+        const int rp = par(po[p]), rq = par(po[q]);
         if (rp == rq) continue;
         const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
         atomicMax(best_rel + rp, key);
@@ -98,13 +98,14 @@ __global__ void edge_max(int H, int W, int F, const double* __restrict__ rel, co
 }
 
 // pass 2: among the edges at that reliability, the smallest id
-__global__ void edge_argmin(int H, int W, int F, const double* __restrict__ rel, const int* __restrict__ parent,
+__global__ void edge_argmin(int H, int W, int F, const double* __restrict__ rel,
+                            const unsigned long long* __restrict__ po,
                             const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
     const size_t ne = 2 * (size_t)H * W * F;
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x) {
         int p, q;
         if (!edge_ends((unsigned)e, H, W, p, q)) continue;
-        const int rp = parent[p], rq = parent[q];
+        const int rp = par(po[p]), rq = par(po[q]);
         if (rp == rq) continue;
         const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
         if (key == best_rel[rp]) atomicMin(best_id + rp, (unsigned)e);
@@ -118,42 +119,90 @@ __device__ __forceinline__ int edge_k(const float* __restrict__ w, int a, int b)
     return (int)rint(__ddiv_rn(__dsub_rn(gam(dw), dw), 6.283185307179586));
 }
 
-// roots hook onto the root across their best edge (reads parent/off, writes parent2/off2)
-__global__ void hook(int H, int W, int F, const float* __restrict__ w, const int* __restrict__ parent,
-                     const int* __restrict__ off, const unsigned* __restrict__ best_id, int* __restrict__ parent2,
-                     int* __restrict__ off2, int* __restrict__ hooked) {
-    const size_t n = (size_t)H * W * F;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int c = (int)i;
-        int np = parent[c], no = off[c];
-        if (np == c && best_id[c] != 0xffffffffu) {
+// ---- root lists: after the first rounds most nodes are not roots, so the per-round work that
+// only concerns roots (reset, hook, compression of the root chains) runs over a compact list
+// of the current roots; one full pass then re-links every node to its new root.
+__global__ void init_list(size_t n, unsigned* list, unsigned* count) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        list[i] = (unsigned)i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned)n;
+}
+__global__ void reset_best_list(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
+                                unsigned long long* best_rel, unsigned* best_id) {
+    const unsigned n = *count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned r = list[k];
+        best_rel[r] = 0ull;
+        best_id[r] = 0xffffffffu;
+    }
+}
+// roots hook onto the root across their best edge; the new entry goes to staged[c] (the
+// best_rel slot of root c, no longer needed) so that roots read each other's old entries
+__global__ void hook_list(int H, int W, const float* __restrict__ w, const unsigned* __restrict__ list,
+                          const unsigned* __restrict__ count, const unsigned long long* __restrict__ po,
+                          const unsigned* __restrict__ best_id, unsigned long long* staged, int* hooked) {
+    const unsigned n = *count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int c = (int)list[k];
+        unsigned long long out = po[c];
+        if (best_id[c] != 0xffffffffu) {
             const unsigned e = best_id[c];
             int p, q;
             edge_ends(e, H, W, p, q);
-            const int pc = parent[p] == c ? p : q;
-            const int po = pc == p ? q : p;
-            const int d = parent[po];
+            const unsigned long long wp = po[p], wq = po[q];
+            const bool pin = par(wp) == c;
+            const int pc = pin ? p : q, oth = pin ? q : p;
+            const unsigned long long wc = pin ? wp : wq, wo = pin ? wq : wp;
+            const int d = par(wo);
             const bool mutual = best_id[d] == e;
             if (!(mutual && d < c)) {                 // of a mutual pair the smaller id stays root
-                np = d;
-                no = off[po] - off[pc] - edge_k(w, pc, po);
+                out = pk(d, ofs(wo) - ofs(wc) - edge_k(w, pc, oth));
                 *hooked = 1;
             }
         }
-        parent2[c] = np;
-        off2[c] = no;
+        staged[c] = out;
     }
 }
-
-// pointer jumping: parent ← parent(parent), off ← off + off(parent)
-__global__ void jump(size_t n, const int* __restrict__ parent, const int* __restrict__ off, int* __restrict__ parent2,
-                     int* __restrict__ off2, int* __restrict__ changed) {
+__global__ void apply_list(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
+                           const unsigned long long* __restrict__ staged, unsigned long long* po) {
+    const unsigned n = *count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned c = list[k];
+        po[c] = staged[c];
+    }
+}
+__global__ void jump_list(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
+                          unsigned long long* po, int* __restrict__ changed) {
+    const unsigned n = *count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned i = list[k];
+        const unsigned long long wi = po[i];
+        const int p = par(wi);
+        const unsigned long long wp = __ldcg(po + p);
+        const int pp = par(wp);
+        if (pp != p) {
+            po[i] = pk(pp, ofs(wi) + ofs(wp));
+            *changed = 1;
+        }
+    }
+}
+// every node: (old root r, off) → (root(r), off + off(r)); roots' entries already point at
+// their final roots (after jump_list), and only roots' entries are read, so one pass suffices
+__global__ void relink_all(size_t n, unsigned long long* po) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int p = parent[i];
-        const int pp = parent[p];
-        parent2[i] = pp;
-        off2[i] = off[i] + off[p];
-        if (pp != p) *changed = 1;
+        const unsigned long long wi = po[i];
+        const int p = par(wi);
+        const unsigned long long wp = po[p];
+        const int pp = par(wp);
+        if (pp != p) po[i] = pk(pp, ofs(wi) + ofs(wp));
+    }
+}
+__global__ void compact_roots(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
+                              const unsigned long long* __restrict__ po, unsigned* out, unsigned* out_count) {
+    const unsigned n = *count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned c = list[k];
+        if (par(po[c]) == (int)c) out[atomicAdd(out_count, 1u)] = c;
     }
 }
 
@@ -211,13 +260,13 @@ __global__ void anchor_argmin(size_t plane, int f0, const double* __restrict__ r
     }
 }
 
-__global__ void finish(size_t plane, int F, const float* __restrict__ w, const int* __restrict__ off,
+__global__ void finish(size_t plane, int F, const float* __restrict__ w, const unsigned long long* __restrict__ po,
                        const unsigned* idx, float* __restrict__ out) {
     const size_t n = plane * F;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const int k0 = off[idx[i / plane]];
+        const int k0 = ofs(po[idx[i / plane]]);
         const float v = w[i];
-        out[i] = isfinite(v) ? (float)((double)v + 6.283185307179586 * (double)(off[i] - k0)) : v;
+        out[i] = isfinite(v) ? (float)((double)v + 6.283185307179586 * (double)(ofs(po[i]) - k0)) : v;
     }
 }
 
@@ -225,10 +274,11 @@ size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Ws {
     double* rel;
-    int *parent, *off, *parent2, *off2;
+    unsigned long long* po;           // packed (parent, 2π offset) nodes
+    unsigned *list, *list2;           // current roots / next round's roots
     unsigned long long* best_rel;
     unsigned* best_id;
-    int* flags;                  // [0] hooked, [1] changed
+    int* flags;                  // [0] hooked, [1] changed, [2] scratch, [4] / [5] list counts
     unsigned long long* amax;
     unsigned* aidx;
 };
@@ -241,21 +291,19 @@ size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
         return p;
     };
     char* r = take(n * sizeof(double));
-    char* p1 = take(n * sizeof(int));
-    char* o1 = take(n * sizeof(int));
-    char* p2 = take(n * sizeof(int));
-    char* o2 = take(n * sizeof(int));
+    char* p1 = take(n * sizeof(unsigned long long));
+    char* l1 = take(n * sizeof(unsigned));
+    char* l2 = take(n * sizeof(unsigned));
     char* br = take(n * sizeof(unsigned long long));
     char* bi = take(n * sizeof(unsigned));
-    char* fl = take(4 * sizeof(int));
+    char* fl = take(8 * sizeof(int));
     char* am = take(F * sizeof(unsigned long long));
     char* ai = take(F * sizeof(unsigned));
     if (ws) {
         ws->rel = (double*)r;
-        ws->parent = (int*)p1;
-        ws->off = (int*)o1;
-        ws->parent2 = (int*)p2;
-        ws->off2 = (int*)o2;
+        ws->po = (unsigned long long*)p1;
+        ws->list = (unsigned*)l1;
+        ws->list2 = (unsigned*)l2;
         ws->best_rel = (unsigned long long*)br;
         ws->best_id = (unsigned*)bi;
         ws->flags = (int*)fl;
@@ -312,28 +360,34 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
         const float* w = wrapped + (size_t)f0 * plane;
         float* out = unwrapped + (size_t)f0 * plane;
         reliability_kernel<<<gn, 256, 0, s>>>(w, H, W, nf, ws.rel);
-        init_kernel<<<gn, 256, 0, s>>>(n, ws.parent, ws.off);
+        init_kernel<<<gn, 256, 0, s>>>(n, ws.po);
+        unsigned* cnt = reinterpret_cast<unsigned*>(ws.flags + 4);
+        unsigned* cnt2 = reinterpret_cast<unsigned*>(ws.flags + 5);
+        init_list<<<gn, 256, 0, s>>>(n, ws.list, cnt);
         for (int round = 0; round < 64; ++round) {                    // Borůvka: ≤ log2(n) rounds
-            reset_best<<<gn, 256, 0, s>>>(n, ws.best_rel, ws.best_id);
-            edge_max<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.parent, ws.best_rel);
-            edge_argmin<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.parent, ws.best_rel, ws.best_id);
+            reset_best_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.best_rel, ws.best_id);
+            edge_max<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel);
+            edge_argmin<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel, ws.best_id);
             if (cudaMemsetAsync(ws.flags, 0, 2 * sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
-            hook<<<gn, 256, 0, s>>>(H, W, nf, w, ws.parent, ws.off, ws.best_id, ws.parent2, ws.off2, ws.flags);
-            std::swap(ws.parent, ws.parent2);
-            std::swap(ws.off, ws.off2);
-            for (int j = 0; j < 64; j += 2) {                             // compress to the roots
+            hook_list<<<gn, 256, 0, s>>>(H, W, w, ws.list, cnt, ws.po, ws.best_id, ws.best_rel, ws.flags);
+            apply_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.best_rel, ws.po);
+            for (int j = 0; j < 64; j += 2) {                             // compress the root chains
+                // two in-place jumps per readback; the flag records only the second, so a pass
+                // that changed nothing ends the compression
+                jump_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.po, ws.flags + 2);
                 if (cudaMemsetAsync(ws.flags + 1, 0, sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
-                for (int t = 0; t < 2; ++t) {                             // two jumps per readback
-                    jump<<<gn, 256, 0, s>>>(n, ws.parent, ws.off, ws.parent2, ws.off2, ws.flags + 1);
-                    std::swap(ws.parent, ws.parent2);
-                    std::swap(ws.off, ws.off2);
-                }
+                jump_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.po, ws.flags + 1);
                 if (cudaMemcpyAsync(host_flags, ws.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                     cudaStreamSynchronize(s) != cudaSuccess)
                     return BOS_ERR_CUDA;
                 if (!host_flags[1]) break;
             }
             if (!host_flags[0]) break;                                  // nothing hooked: one tree per frame
+            relink_all<<<gn, 256, 0, s>>>(n, ws.po);
+            if (cudaMemsetAsync(cnt2, 0, sizeof(unsigned), s) != cudaSuccess) return BOS_ERR_CUDA;
+            compact_roots<<<gn, 256, 0, s>>>(ws.list, cnt, ws.po, ws.list2, cnt2);
+            std::swap(ws.list, ws.list2);
+            std::swap(cnt, cnt2);
         }
         if (cudaMemsetAsync(ws.amax, 0, nf * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(ws.aidx, 0xff, nf * sizeof(unsigned), s) != cudaSuccess)
@@ -343,7 +397,7 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
             anchor_max<<<ga, 256, 0, s>>>(plane, a0, ws.rel, ws.amax);
             anchor_argmin<<<ga, 256, 0, s>>>(plane, a0, ws.rel, ws.amax, ws.aidx);
         }
-        finish<<<gn, 256, 0, s>>>(plane, nf, w, ws.off, ws.aidx, out);
+        finish<<<gn, 256, 0, s>>>(plane, nf, w, ws.po, ws.aidx, out);
         if (cudaGetLastError() != cudaSuccess) return BOS_ERR_CUDA;
     }
     return cudaStreamSynchronize(s) == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
