@@ -485,6 +485,12 @@ __device__ __forceinline__ int power_iteration_fb(const float (&Rd)[M], const cx
     bool oka = false;
     float l0, l1;
     int n = power_iteration<M, false>(Rd, Ro, u, ok, l0);
+    // R is PSD: if the converged eigenvalue exceeds half the trace no other eigenvalue can be
+    // larger, so the tone start already found the top eigenvector (the usual case)
+    float trace = 0.0f;
+#pragma unroll
+    for (int i = 0; i < M; ++i) trace += Rd[i];
+    if (ok && l0 > 0.5005f * trace) return n;
     n += power_iteration<M, true>(Rd, Ro, ua, oka, l1);
     if (l1 > l0) {
 #pragma unroll
