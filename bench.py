@@ -129,9 +129,12 @@ def init_dist():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # BOS_DIST_BACKEND=gloo: functional check of the N>1 code path on a single-GPU box (ranks
+        # share the device; never a measurement)
+        backend = os.environ.get("BOS_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
             dist.init_process_group(backend, device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
@@ -192,7 +195,7 @@ def run_cuda(args, world, rank, local):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py --impl cuda needs a CUDA device (no CPU fallback)")
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     bosrm.lib()
     M = args.window_len
@@ -238,7 +241,7 @@ def run_cuda(args, world, rank, local):
     torch.cuda.synchronize()
     if sharding.is_dist():
         dist.barrier()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     sampler.start()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
