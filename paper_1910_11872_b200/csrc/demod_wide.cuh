@@ -29,6 +29,14 @@ namespace bos {
 #define BOS_WIDE_MIN_M 21
 #endif
 constexpr int kWideMinM = BOS_WIDE_MIN_M;
+// unroll factor of the warp kernel's per-root loops (Horner over N, reciprocal sums over K):
+// code size against loop overhead (the kernel showed instruction-fetch stalls)
+// (measured: unroll 8 → M = 21 +8 %, M = 24 +16 %; no gain at M = 28, 32 → full unroll there)
+#ifndef BOS_WIDE_UNROLL
+#define BOS_WIDE_UNROLL 8
+#endif
+template <int N>
+constexpr int wide_unroll() { return N <= 2 * 24 - 2 ? BOS_WIDE_UNROLL : 64; }
 template <bool FB>
 constexpr int wide_min_m() { return FB ? (BOS_WIDE_MIN_M < 19 ? BOS_WIDE_MIN_M : 19) : BOS_WIDE_MIN_M; }
 
@@ -63,7 +71,7 @@ __device__ __forceinline__ float2 newton_ratio_smem(const cx2* __restrict__ c, f
     const cx2 Vj = mul2(cx2_make(v.y, v.x), cx2_make(-1.0f, 1.0f));
     cx2 p = c[N];
     cx2 dp = 0ull;
-#pragma unroll
+#pragma unroll (wide_unroll<N>())
     for (int k = N - 1; k >= 0; --k) {
         dp = cmad2(dp, V, Vj, p);
         p = cmad2(p, V, Vj, c[k]);
@@ -83,7 +91,7 @@ __device__ __forceinline__ float2 newton_on_derivative_smem(const cx2* __restric
     const cx2 Vj = mul2(cx2_make(z.y, z.x), cx2_make(-1.0f, 1.0f));
     cx2 p = c[N];
     cx2 dp = 0ull, ddp = 0ull;
-#pragma unroll
+#pragma unroll (wide_unroll<N>())
     for (int k = N - 1; k >= 0; --k) {
         ddp = cmad2(ddp, V, Vj, dp);
         dp = cmad2(dp, V, Vj, p);
@@ -428,7 +436,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             const bool near = fabsf(1.0f - cabs2(z)) < kNearCircle;
                             const cx2 ziC = mul2(zp, kPosNeg);
                             cx2 s = 0ull;
-#pragma unroll
+#pragma unroll (wide_unroll<N>())
                             for (int j = 0; j < K; ++j) {
                                 // 1/(z − z_j) = conj(d)/|d|²; the own term gets |d|² = ∞ → 0
                                 const cx2 d1 = fma2(va[j], kNegPos, ziC);
