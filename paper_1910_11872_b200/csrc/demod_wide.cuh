@@ -35,8 +35,11 @@ constexpr int kWideMinM = BOS_WIDE_MIN_M;
 #ifndef BOS_WIDE_UNROLL
 #define BOS_WIDE_UNROLL 8
 #endif
+#ifndef BOS_WIDE_UNROLL_MAX_M
+#define BOS_WIDE_UNROLL_MAX_M 24
+#endif
 template <int N>
-constexpr int wide_unroll() { return N <= 2 * 24 - 2 ? BOS_WIDE_UNROLL : 64; }
+constexpr int wide_unroll() { return N <= 2 * BOS_WIDE_UNROLL_MAX_M - 2 ? BOS_WIDE_UNROLL : 64; }
 template <bool FB>
 constexpr int wide_min_m() { return FB ? (BOS_WIDE_MIN_M < 19 ? BOS_WIDE_MIN_M : 19) : BOS_WIDE_MIN_M; }
 
