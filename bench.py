@@ -344,8 +344,11 @@ def run_cuda(args, world, rank, local):
         valid = (ofl & R.PARITY_EXCLUDE_MASK) == 0
         e = R.wrap(g - o)[valid]
         e = e[np.isfinite(e)]
+        gfl = flags[1:F + 1].cpu().numpy()[:, pix[0], pix[1]]
+        gpu_only = ((gfl & R.PARITY_EXCLUDE_MASK) != 0) & valid     # flagged by the GPU, not the oracle
         parity = {"rms": float(math.sqrt(np.mean(e * e))), "max": float(np.max(np.abs(e))), "n": int(e.size),
-                  "excluded_frac": float(1 - valid.mean()), "tol": {"rms": 1e-3, "max": 1e-2}}
+                  "excluded_frac": float(1 - valid.mean()), "gpu_only_flagged_frac": float(gpu_only.mean()),
+                  "tol": {"rms": 1e-3, "max": 1e-2}}
 
     if rank == 0:
         line = {

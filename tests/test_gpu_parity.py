@@ -50,8 +50,9 @@ def test_c1_full_frame_parity_and_closed_form(M):
     f = synth.make_frame(w, 0)
     g, gfl = run_gpu(f, M)
     o, ofl = R.demod_frame(f.numpy(), M)
-    s = assert_parity(g, o, ofl, f"C1 M={M}", max_excluded_frac=0.0)
+    s = assert_parity(g, o, ofl, f"C1 M={M}", max_excluded_frac=0.0, gpu_flags=gfl)
     assert s["n"] == 256 * 256
+    assert s["gpu_only_flagged_frac"] == 0.0
     truth = synth.true_phase(w, 0).numpy()
     m = _interior(256, 256, M)
     assert np.abs(R.wrap(g - truth))[m].max() <= 1e-3
@@ -101,7 +102,8 @@ def test_all_window_lengths_ragged_frame(M):
     o, ofl = R.demod_frame(f.numpy(), M)
     # for M ≥ 17 almost every window of this small frame is clamped (repeated rows/columns),
     # which the oracle more often flags (AMBIGUOUS / SMALL_GAP)
-    assert_parity(g, o, ofl, f"ragged M={M}", max_excluded_frac=0.05 if M < 17 else 0.15)
+    s = assert_parity(g, o, ofl, f"ragged M={M}", max_excluded_frac=0.05 if M < 17 else 0.15, gpu_flags=gfl)
+    assert s["gpu_only_flagged_frac"] <= 0.01, s
     assert np.all((gfl & bosrm.FLAG_BORDER) == (ofl & R.FLAG_BORDER))
     del w
 
