@@ -242,7 +242,9 @@ __device__ __forceinline__ int power_iteration_warp_fb(const cx2 (&R)[M], int la
 #define BOS_WIDE_BLOCKS 0
 #endif
 template <int M>
-constexpr int wide_min_blocks() { return BOS_WIDE_BLOCKS > 0 ? BOS_WIDE_BLOCKS : (M <= 24 ? 3 : 2); }
+constexpr int wide_min_blocks() {   // measured: 4 CTAs/SM best up to M = 24 (no spills), 3 at 25, 2 above
+    return BOS_WIDE_BLOCKS > 0 ? BOS_WIDE_BLOCKS : (M <= 24 ? 4 : (M <= 25 ? 3 : 2));
+}
 
 template <int M, bool COUNT, bool FB = false>
 __global__ void __launch_bounds__(kThreads, wide_min_blocks<M>())
