@@ -602,9 +602,11 @@ __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const 
 }
 
 // CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).
+// (measured per M on C4: 4 CTAs/SM up to M = 9, 3 for M = 10, 11, 2 for 12, 13 — one more CTA
+// costs 4–27 % at M = 10, 12, 13 through spills, one fewer is slower everywhere)
 template <int M>
 constexpr int min_blocks_per_sm() {
-    return M <= 8 ? 4 : (M <= 10 ? 3 : (M <= 13 ? 2 : 1));
+    return M <= 9 ? 4 : (M <= 11 ? 3 : (M <= 13 ? 2 : 1));
 }
 
 template <int M, bool COUNT, bool FB = false>
