@@ -30,13 +30,14 @@ namespace bos {
 #endif
 constexpr int kWideMinM = BOS_WIDE_MIN_M;
 // unroll factor of the warp kernel's per-root loops (Horner over N, reciprocal sums over K):
-// code size against loop overhead (the kernel showed instruction-fetch stalls)
-// (measured: unroll 8 → M = 21 +8 %, M = 24 +16 %; no gain at M = 28, 32 → full unroll there)
+// unroll 8 instead of full unrolling shrinks the code (the kernel showed instruction-fetch
+// stalls) and the registers (≤ 128 → 4 CTAs/SM without spills): M = 21 +6 %, 24 +4 %, 25…32
+// +12…16 % over full unroll with 2–3 CTAs/SM
 #ifndef BOS_WIDE_UNROLL
 #define BOS_WIDE_UNROLL 8
 #endif
 #ifndef BOS_WIDE_UNROLL_MAX_M
-#define BOS_WIDE_UNROLL_MAX_M 24
+#define BOS_WIDE_UNROLL_MAX_M 32
 #endif
 template <int N>
 constexpr int wide_unroll() { return N <= 2 * BOS_WIDE_UNROLL_MAX_M - 2 ? BOS_WIDE_UNROLL : 64; }
@@ -242,8 +243,8 @@ __device__ __forceinline__ int power_iteration_warp_fb(const cx2 (&R)[M], int la
 #define BOS_WIDE_BLOCKS 0
 #endif
 template <int M>
-constexpr int wide_min_blocks() {   // measured: 4 CTAs/SM best up to M = 24 (no spills), 3 at 25, 2 above
-    return BOS_WIDE_BLOCKS > 0 ? BOS_WIDE_BLOCKS : (M <= 24 ? 4 : (M <= 25 ? 3 : 2));
+constexpr int wide_min_blocks() {   // measured: 4 CTAs/SM (≤ 128 registers, no spills) best for M = 21…32
+    return BOS_WIDE_BLOCKS > 0 ? BOS_WIDE_BLOCKS : 4;
 }
 
 template <int M, bool COUNT, bool FB = false>
