@@ -604,13 +604,13 @@ __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const 
 // CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).
 // (measured per M on C4: 4 CTAs/SM up to M = 9, 3 for M = 10, 11, 2 for 12, 13 — one more CTA
 // costs 4–27 % at M = 10, 12, 13 through spills, one fewer is slower everywhere)
-template <int M>
-constexpr int min_blocks_per_sm() {
-    return M <= 9 ? 4 : (M <= 11 ? 3 : (M <= 13 ? 2 : 1));
+template <int M, bool FB = false>
+constexpr int min_blocks_per_sm() {   // FB holds more state: its own (earlier) table — M = 11 FB: 1237 vs 1073 at 3 CTAs
+    return FB ? (M <= 8 ? 4 : (M <= 10 ? 3 : (M <= 13 ? 2 : 1))) : (M <= 9 ? 4 : (M <= 11 ? 3 : (M <= 13 ? 2 : 1)));
 }
 
 template <int M, bool COUNT, bool FB = false>
-__global__ void __launch_bounds__(kThreads, min_blocks_per_sm<M>())
+__global__ void __launch_bounds__(kThreads, min_blocks_per_sm<M, FB>())
 demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
              const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
              float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
