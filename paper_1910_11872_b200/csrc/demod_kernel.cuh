@@ -1,10 +1,12 @@
 // demod_kernel.cuh — sm_100a windowed root-MUSIC demodulation kernel (thread per pixel).
 //
-// One CTA = a 32×4 pixel tile of one frame.  The CTA stages the (4+M−1)×(32+M−1) complex
-// window halo of its tile in shared memory once (every HBM byte of the frame is read once
-// per frame, the overlap between the M² windows of neighbouring pixels is served from
-// SMEM), then each thread runs the whole per-pixel chain of Algorithm 1 in
-// registers, fused with the reference-phase difference and the flag store:
+// Window sizes M ≤ 20 (the warp kernel, demod_wide.cuh, takes 21…32).  One CTA = 4 warps on
+// a 32-column strip walking (frame, 4-row block) work items; each warp stages the clamped
+// M×(32+M−1) halo rows of its image row in shared memory (cp.async-prefetched one item ahead
+// for M ≤ 15; the M² windows of neighbouring pixels overlap in SMEM, HBM is read about once),
+// then each thread runs the whole per-pixel chain of Algorithm 1 in registers
+// (R_y's triangle in per-thread shared-memory slices for M = 17…20), fused with the
+// reference-phase difference and the flag store:
 //
 //   a2  R_y = Γ_w Γ_w^H (lower triangle, FP32)                            Eq.(4)
 //   a3  u_1: power iteration on R_y from the lag-1 tone estimate; v_1 ∝ Γ_w^H u_1

@@ -1,4 +1,5 @@
-// demod_wide.cuh — warp-per-pixel root-MUSIC demodulation for large windows (M = 19…32 by default).
+// demod_wide.cuh — warp-per-pixel root-MUSIC demodulation for large windows (M = 21…32 by default;
+// the FB variant from 19).
 //
 // Same algorithm and arithmetic as demod_kernel.cuh (a1–a7, symmetric Aberth, Newton polish),
 // laid out for M where a thread can no longer hold R_y (M(M+1)/2 complex) in registers:
@@ -13,8 +14,9 @@
 //   vectors and warp shuffles; the polynomial coefficients go to a per-warp SMEM buffer that
 //   every lane reads by broadcast during Horner;
 // * Aberth: lane k owns tracked root z_k (K = M−1 ≤ 31 roots), simultaneous (Jacobi) update,
-//   the other roots and mirrors arrive by shuffle; warp-reduced stop test, argmin selection
-//   and margin; two Newton polish steps on the selected root;
+//   the other roots and mirrors arrive through per-warp SMEM buffers; warp-reduced stop test,
+//   argmin selection and margin; Newton polish of the selected root with the whole warp;
+// * per-root loops unrolled 8× (≤ 128 registers → 4 CTAs/SM without spills);
 // * Eq.(15) row sums per lane, warp reduction, lane 0 stores phase + flags.
 #pragma once
 
