@@ -294,9 +294,10 @@ def test_c5_full_stack_on_one_gpu():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("M", [24, 32])
+@pytest.mark.parametrize("M", [12, 15, 17, 20, 21, 24, 25, 32])
 def test_c4_large_windows_sampled_parity(M):
-    """C4 frames (2048², diffusion flow, 10 dB) at large windows: 2048 random pixels of frame 7,
+    """C4 frames (2048², diffusion flow, 10 dB) at every kernel regime: registers (12, 15),
+    R_y in shared memory (17, 20), warp kernel (21, 24, 25, 32): 2048 random pixels of frame 7,
     plus the near-tie pixel (2, 255) where the runner-up root must be refined (M = 32)."""
     w = synth.workload("C4")
     frames = synth.make_stack(w, frames=[0, 7], device=DEV)
