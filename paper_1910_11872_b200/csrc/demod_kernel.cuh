@@ -512,12 +512,20 @@ __device__ __forceinline__ int power_iteration_fb(const float (&Rd)[M], const cx
 #endif
 template <int M, bool FB>
 constexpr bool kRsmem() { return !FB && M >= BOS_RSMEM_MIN_M && M <= 20; }
-template <int M>
-constexpr int rsmem_split() {          // first row of the second pass: ≈ half the triangle's entries each
+// row boundaries of the register-blocked passes: P passes of ≈ equal entry counts
+template <int M, int P, int B>
+constexpr int rsmem_bound() {          // first row of pass B (B = 0 … P; bound P = M)
+    if (B <= 0) return 1;
+    if (B >= P) return M;
     int r = 1, acc = 0;
-    while (r < M && 2 * (acc + r) <= M * (M - 1) / 2) acc += r++;
+    const int target = (M * (M - 1) / 2) * B / P;
+    while (r < M && acc + r <= target) acc += r++;
     return r;
 }
+// 4 passes (≈ M(M−1)/8 accumulators each): M = 18 +16 %, 19 +11 %, 20 +11 % over 2 passes
+#ifndef BOS_RSMEM_PASSES
+#define BOS_RSMEM_PASSES 4
+#endif
 
 // Rows [LO, HI) of the strict lower triangle of R_y (entries R_ij, j < i) accumulated over the
 // M columns of the window in registers, then stored to the thread's shared-memory slice.
@@ -714,8 +722,11 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         Rd[i] = fmaf(g.x, g.x, fmaf(g.y, g.y, Rd[i]));
                     }
                 }
-                cov_pass_smem<M, TW, 1, rsmem_split<M>()>(win, Rs);
-                cov_pass_smem<M, TW, rsmem_split<M>(), M>(win, Rs);
+                constexpr int P = BOS_RSMEM_PASSES;
+                cov_pass_smem<M, TW, rsmem_bound<M, P, 0>(), rsmem_bound<M, P, 1>()>(win, Rs);
+                cov_pass_smem<M, TW, rsmem_bound<M, P, 1>(), rsmem_bound<M, P, 2>()>(win, Rs);
+                if constexpr (P >= 3) cov_pass_smem<M, TW, rsmem_bound<M, P, 2>(), rsmem_bound<M, P, 3>()>(win, Rs);
+                if constexpr (P >= 4) cov_pass_smem<M, TW, rsmem_bound<M, P, 3>(), rsmem_bound<M, P, 4>()>(win, Rs);
             } else {
 #pragma unroll
             for (int t = 0; t < NOFF; ++t) Ro[t] = 0ull;
