@@ -49,8 +49,12 @@ constexpr float kPowerTol = BOS_POWER_TOL;    // ‖u_{k+1} − u_k‖² stop (e
 // step: an approximation repelled by its neighbours can take small steps far from any root
 // (the repulsion term balances P/P′), and the loose stop then misses the root it is heading
 // for.  Seen with the FB variant's polynomials (clamped border windows); always on there.
-// The paper path keeps the plain step test (−11 % throughput at 10 dB otherwise; DESIGN.md
-// §6 measures how often the two differ); BOS_STOP_NEWTON_PAPER=1 turns it on there too.
+// The paper path needs it too: tools/stress_parity.py (random M, frame sizes, 0–40 dB and
+// noise-free) found loose-stop misplacements at M = 17–20 (one noise-free) and, at −5 dB,
+// M = 8 and 16.  It is compile-time on from M = BOS_STOP_NEWTON_MIN_M (12; cost ≤ 3 % there)
+// and in the warp kernel (cost within noise); below, where it would cost 7 % at 10 dB (warps
+// wait for their slowest lane), it is switched on per pixel for weak-tone windows only
+// (λ1 < kLowSnrRatio·tr R_y, see below).  BOS_STOP_NEWTON_PAPER=1 forces it everywhere.
 #ifndef BOS_PREFETCH
 #define BOS_PREFETCH 1
 #endif
@@ -72,8 +76,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef BOS_STOP_NEWTON_PAPER
 #define BOS_STOP_NEWTON_PAPER 0
 #endif
-template <bool FB>
-constexpr bool newton_stop() { return FB || BOS_STOP_NEWTON_PAPER != 0; }
+#ifndef BOS_STOP_NEWTON_MIN_M
+#define BOS_STOP_NEWTON_MIN_M 12
+#endif
+template <bool FB, int M>
+constexpr bool newton_stop() { return FB || BOS_STOP_NEWTON_PAPER != 0 || M >= BOS_STOP_NEWTON_MIN_M; }
 constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 // Loose sweep stop max_i |Δz_i|² < tol, then the Newton polish of the selected root.  The
 // thread kernel (Gauss–Seidel sweeps) uses 2e-3 (|Δz| < 0.045): a warp runs as many sweeps as
@@ -85,7 +92,29 @@ constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 #define BOS_ABERTH_TOL2 2e-3f
 #endif
 constexpr float kAberthTol2 = BOS_ABERTH_TOL2;  // thread kernel (demod_kernel, demod_ss)
-constexpr float kAberthTol2Wide = 1e-3f;       // warp kernel (demod_wide)
+#ifndef BOS_ABERTH_TOL2_WIDE
+#define BOS_ABERTH_TOL2_WIDE 1e-3f
+#endif
+constexpr float kAberthTol2Wide = BOS_ABERTH_TOL2_WIDE;   // warp kernel (demod_wide)
+// Warp kernel, paper path: windows whose dominant eigenvalue λ1 is below kLowSnrRatio·tr(R_y)
+// (a weak tone: λ1/tr ≈ (M·SNR + 1)/(M·(SNR + 1)), ≈ 0.91 at 10 dB, ≈ 0.5 at 0 dB) start from
+// the tighter kAberthLowSnrTol2 — their polynomials have many roots near the unit circle and
+// the loose stop misplaced the selected one in 5 of 400 random 0–5 dB cases at M ≥ 27
+// (tools/stress_parity.py); the test is per pixel and warp-uniform, so ≥ 10 dB work is unchanged.
+#ifndef BOS_LOWSNR_RATIO
+#define BOS_LOWSNR_RATIO 0.9f
+#endif
+constexpr float kLowSnrRatio = BOS_LOWSNR_RATIO;
+// Thread kernel, M < BOS_STOP_NEWTON_MIN_M: λ1 below this fraction of tr(R_y) switches the
+// Newton-ratio stop on for that pixel (see newton_stop).
+#ifndef BOS_WEAK_NEWTON_RATIO
+#define BOS_WEAK_NEWTON_RATIO 0.7f
+#endif
+constexpr float kWeakNewtonRatio = BOS_WEAK_NEWTON_RATIO;
+#ifndef BOS_WEAK_MODE
+#define BOS_WEAK_MODE 1     // 1: weak pixels start from kAberthLowSnrTol2; 0: per-pixel Newton-ratio stop
+#endif
+constexpr float kAberthLowSnrTol2 = 1e-4f;
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;
@@ -115,6 +144,7 @@ enum : uint8_t {
     kFlagLowAmplitude = 1u << 3,
     kFlagNonfinite = 1u << 4,
     kFlagBorder = 1u << 5,
+    kFlagWeakInternal = 1u << 7,   // thread kernel scratch bit (weak-tone window), cleared before the store
 };
 
 // ---------------------------------------------------------------- complex helpers (FP32)
@@ -230,7 +260,8 @@ __device__ __forceinline__ cx2 mirror(cx2 z) {
 // root update.  Complex values are packed (cx2.cuh): Horner and the reciprocal sum run on
 // FFMA2.  Returns the number of sweeps; `ok` = converged or stagnated at FP32 noise.
 template <int N, bool NEWTON_STOP = false>
-__device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2], bool& ok, float tol2) {
+__device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2], bool& ok, float tol2,
+                                          bool nstop = false) {
     constexpr int K = N / 2;
     cx2 zm[K];
 #pragma unroll
@@ -280,7 +311,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
             }
             const cx2 zn = cx2_make(zi.x - w.x, zi.y - w.y);
             maxw = fmaxf(maxw, w2);
-            if (NEWTON_STOP && !near) parked |= !(cabs2(num) < tol2 * cabs2(den));   // near: the P′ step is the test
+            if ((NEWTON_STOP || nstop) && !near) parked |= !(cabs2(num) < tol2 * cabs2(den));   // near: the P′ step is the test
 #pragma unroll
             for (int j = 0; j + 1 < K; ++j) {
                 z[j] = z[j + 1];
@@ -783,6 +814,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             t = cmul(t, e);
                         }
                     }
+                    float lam2 = CUDART_INF_F;   // ‖R u‖² of the converged step (λ1²); set at the break only
                     for (n_pow = 0; n_pow < kPowerMaxIt;) {
                         // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
                         cx2 uj[M];
@@ -816,8 +848,10 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             u[i] = yn;
                         }
                         ++n_pow;
-                        if (diff < kPowerTol) { pow_ok = true; break; }
+                        if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
                     }
+                    if constexpr (!newton_stop<FB, M>())   // weak-tone window (see newton_stop); a flag bit, not a register
+                        if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
                     }
                     // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
                     cx2 unj[M];
@@ -875,10 +909,10 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     int its = 0;
                     float marg = CUDART_INF_F;
                     float2 zs, z2;
-                    float tol2 = kAberthTol2;
+                    float tol2 = (BOS_WEAK_MODE == 1 && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
 #pragma unroll 1
                     for (int attempt = 0;; ++attempt) {
-                        its += aberth_sym<N, newton_stop<FB>()>(c, z, ok, tol2);
+                        its += aberth_sym<N, newton_stop<FB, M>()>(c, z, ok, tol2, BOS_WEAK_MODE == 0 && (fl & kFlagWeakInternal));
                         zs = select_root<N / 2>(z, marg, z2);
                         // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
                         // ~1e-5 there); Newton steps on the selected root alone then make it
@@ -968,7 +1002,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
             }
             const size_t o = (size_t)f * plane + (size_t)py * W + px;
             out[o] = result;
-            if (flags != nullptr) flags[o] = fl;
+            if (flags != nullptr) flags[o] = fl & uint8_t(~kFlagWeakInternal);
             if (omx != nullptr) omx[o] = wx;
             if (omy != nullptr) omy[o] = wy;
             if (COUNT) {

@@ -350,11 +350,13 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     if (FB) fb_average_rows<M>(R, ri);
                     cx2 u;
                     bool pow_ok = false;
+                    bool weak = false;                          // see kLowSnrRatio
                     if constexpr (FB) {
                         n_pow = power_iteration_warp_fb<M>(R, lane, rl, va, u, pow_ok, trace);
                     } else {
                         float lam;
                         n_pow = power_iteration_warp<M>(R, lane, rl, va, u, pow_ok, lam);
+                        weak = lam < kLowSnrRatio * trace;
                     }
                     cx2 v = 0ull;
                     if (!FB) {
@@ -428,7 +430,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         cx2 zp = f2_cx2(z);
                         int it = 0;
                         bool ok = false;
-                        float tol2 = kAberthTol2Wide;
+                        float tol2 = weak ? kAberthLowSnrTol2 : kAberthTol2Wide;
                         float2 zb, z2;
                         float marg;
                         int sl;
@@ -469,7 +471,7 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             z = csub(z, w);
                             zp = f2_cx2(z);
                             __syncwarp();                      // everyone has read va/vb
-                            const float n2 = (newton_stop<FB>() && kl && !near) ? cabs2(ratio) : 0.0f;   // see newton_stop
+                            const float n2 = (kl && !near) ? cabs2(ratio) : 0.0f;   // Newton-ratio stop always on here (see newton_stop)
                             if (warp_max(fmaxf(w2, n2 < 1e30f ? n2 : CUDART_INF_F)) < tol2) { ok = true; ++it; break; }
                         }
                         // selection: argmin |log2 |z|²| over lanes, margin to a different frequency

@@ -1,0 +1,74 @@
+"""Randomised GPU-vs-oracle parity stress (development tool): random window sizes, SNRs,
+seeds, frame sizes and phase workloads; reports the worst wrapped error over oracle-unflagged
+pixels per case and every case that breaks the north_star bar (RMS 1e-3, max 1e-2 rad).
+
+    python tools/stress_parity.py --cases 200 --seed 1
+"""
+import argparse
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from oracle import rootmusic as R  # noqa: E402
+from paper_1910_11872_b200 import bosrm, synth  # noqa: E402
+
+
+def draw_cases(seed, n):
+    """The random case sequence of a seed: dicts with M, H, W, snr, workload, t, wseed."""
+    rng = np.random.default_rng(seed)
+    for c in range(n):
+        M = int(rng.integers(3, 33))
+        H = int(rng.integers(max(M, 8), 96))
+        W = int(rng.integers(max(M, 8), 120))
+        snr = float(rng.choice([-5.0, 0.0, 5.0, 10.0, 20.0, 40.0, np.inf]))
+        wl = str(rng.choice(["C2", "C3", "C1"]))
+        wseed = int(rng.integers(0, 1 << 30))
+        t = int(rng.integers(1, 5)) if wl != "C1" else 0
+        yield dict(case=c, M=M, H=H, W=W, snr=snr, workload=wl, t=t, wseed=wseed)
+
+
+def run_case(k):
+    """GPU vs oracle on one case; returns (max, rms, nan count, excluded fraction)."""
+    w = synth.workload(k["workload"], H=k["H"], W=k["W"], seed=k["wseed"])
+    f = synth.make_frame(w, k["t"], snr_db=None if k["snr"] == np.inf else k["snr"])
+    g, _ = bosrm.bos_rootmusic_demod(f.to("cuda"), k["M"])
+    torch.cuda.synchronize()
+    o, ofl = R.demod_frame(f.numpy(), k["M"])
+    valid = (ofl & R.PARITY_EXCLUDE_MASK) == 0
+    e = np.abs(R.wrap(g[0].cpu().numpy().astype(np.float64) - o))[valid]
+    nan = int(np.sum(~np.isfinite(e)))
+    e = e[np.isfinite(e)]
+    mx = float(e.max()) if e.size else 0.0
+    rms = float(math.sqrt(np.mean(e * e))) if e.size else 0.0
+    return mx, rms, nan, float(1 - valid.mean())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--budget-s", type=float, default=600.0)
+    args = ap.parse_args()
+    bad, worst, t0, c = [], 0.0, time.time(), -1
+    for k in draw_cases(args.seed, args.cases):
+        if time.time() - t0 > args.budget_s:
+            break
+        c = k["case"]
+        mx, rms, nan, exc = run_case(k)
+        worst = max(worst, mx)
+        if nan or mx > 1e-2 or rms > 1e-3:
+            bad.append(dict(k, max=mx, rms=rms, nan=nan, excluded=exc))
+    print(f"cases run: {c + 1}, failures: {len(bad)}, worst max error {worst:.2e} rad")
+    for b in bad:
+        print(b)
+
+
+if __name__ == "__main__":
+    main()
