@@ -45,6 +45,14 @@ constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyon
 #define BOS_POWER_TOL 1e-8f
 #endif
 constexpr float kPowerTol = BOS_POWER_TOL;    // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2) ≤ 3.3e-4 where σ1²/σ2² ≥ 1.3)
+// Spatial smoothing (demod_ss.cuh): the order-m eigenvector feeds a degree-(2m−2) polynomial
+// whose signal pair is a near-double root, so its angle is far more sensitive to u than at
+// order M; a 3×3…m×m iteration is cheap, so it runs to FP32 noise (stress: 0.01–0.15 rad
+// misses at −5…0 dB with 1e-8).
+#ifndef BOS_POWER_TOL_SS
+#define BOS_POWER_TOL_SS 1e-12f
+#endif
+constexpr float kPowerTolSS = BOS_POWER_TOL_SS;
 // NEWTON_STOP sweeps also require every Newton ratio |P/P′|² < tol2, not only every Aberth
 // step: an approximation repelled by its neighbours can take small steps far from any root
 // (the repulsion term balances P/P′), and the loose stop then misses the root it is heading
@@ -448,7 +456,7 @@ __device__ __forceinline__ void fb_average(float (&Rd)[M], cx2 (&Ro)[M * (M - 1)
 // lam = ‖R u‖ of the last step (the Rayleigh quotient at convergence).
 template <int M, bool RAMP = false>
 __device__ __forceinline__ int power_iteration(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1],
-                                               cx2 (&u)[M], bool& ok, float& lam) {
+                                               cx2 (&u)[M], bool& ok, float& lam, float tol = kPowerTol) {
     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
@@ -502,7 +510,7 @@ __device__ __forceinline__ int power_iteration(const float (&Rd)[M], const cx2 (
             u[i] = yn;
         }
         ++n;
-        if (diff < kPowerTol) { ok = true; break; }
+        if (diff < tol) { ok = true; break; }
     }
     return n;
 }
@@ -513,18 +521,18 @@ __device__ __forceinline__ int power_iteration(const float (&Rd)[M], const cx2 (
 // accepts the runner-up.  Two starts (tone, ramp-weighted tone); the larger ‖R u‖ wins.
 template <int M>
 __device__ __forceinline__ int power_iteration_fb(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1],
-                                                  cx2 (&u)[M], bool& ok) {
+                                                  cx2 (&u)[M], bool& ok, float tol = kPowerTol) {
     cx2 ua[M];
     bool oka = false;
     float l0, l1;
-    int n = power_iteration<M, false>(Rd, Ro, u, ok, l0);
+    int n = power_iteration<M, false>(Rd, Ro, u, ok, l0, tol);
     // R is PSD: if the converged eigenvalue exceeds half the trace no other eigenvalue can be
     // larger, so the tone start already found the top eigenvector (the usual case)
     float trace = 0.0f;
 #pragma unroll
     for (int i = 0; i < M; ++i) trace += Rd[i];
     if (ok && l0 > 0.5005f * trace) return n;
-    n += power_iteration<M, true>(Rd, Ro, ua, oka, l1);
+    n += power_iteration<M, true>(Rd, Ro, ua, oka, l1, tol);
     if (l1 > l0) {
 #pragma unroll
         for (int i = 0; i < M; ++i) u[i] = ua[i];

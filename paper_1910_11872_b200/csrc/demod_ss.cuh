@@ -255,15 +255,15 @@ demod_ss_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, i
                 bool ok_y = false, ok_x = false;
                 float lam;
                 if (FB) fb_average<MS>(Rd, Ro);
-                if (FB) power_iteration_fb<MS>(Rd, Ro, e, ok_y);
-                else power_iteration<MS>(Rd, Ro, e, ok_y, lam);
+                if (FB) power_iteration_fb<MS>(Rd, Ro, e, ok_y, kPowerTolSS);
+                else power_iteration<MS>(Rd, Ro, e, ok_y, lam, kPowerTolSS);
                 float2 u[MS], v[MS];
 #pragma unroll
                 for (int i = 0; i < MS; ++i) u[i] = cx2_f2(e[i]);
                 ss_covariance<MS, true>(win, M, TW, Rd, Ro);
                 if (FB) fb_average<MS>(Rd, Ro);
-                if (FB) power_iteration_fb<MS>(Rd, Ro, e, ok_x);
-                else power_iteration<MS>(Rd, Ro, e, ok_x, lam);
+                if (FB) power_iteration_fb<MS>(Rd, Ro, e, ok_x, kPowerTolSS);
+                else power_iteration<MS>(Rd, Ro, e, ok_x, lam, kPowerTolSS);
 #pragma unroll
                 for (int i = 0; i < MS; ++i) v[i] = cx2_f2(e[i]);
                 // ---- a4 + a5 ----

@@ -227,16 +227,18 @@ __device__ __forceinline__ int power_iteration_warp(const cx2 (&R)[M], int lane,
 // kernel's power_iteration_fb for why one start is not enough under FB averaging).
 template <int M>
 __device__ __forceinline__ int power_iteration_warp_fb(const cx2 (&R)[M], int lane, bool rl, cx2* va, cx2& u,
-                                                       bool& ok, float trace) {
+                                                       bool& ok, float trace, float& lam) {
     cx2 ua;
     bool oka = false;
     float l0, l1;
     int n = power_iteration_warp<M, false>(R, lane, rl, va, u, ok, l0);
+    lam = l0;
     if (ok && l0 > 0.5005f * trace) return n;     // > half the trace of a PSD R: the top one
     n += power_iteration_warp<M, true>(R, lane, rl, va, ua, oka, l1);
     if (l1 > l0) {          // warp-uniform (warp sums)
         u = ua;
         ok = oka;
+        lam = l1;
     }
     return n;
 }
@@ -352,7 +354,9 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     bool pow_ok = false;
                     bool weak = false;                          // see kLowSnrRatio
                     if constexpr (FB) {
-                        n_pow = power_iteration_warp_fb<M>(R, lane, rl, va, u, pow_ok, trace);
+                        float lam;
+                        n_pow = power_iteration_warp_fb<M>(R, lane, rl, va, u, pow_ok, trace, lam);
+                        weak = lam < kLowSnrRatio * trace;
                     } else {
                         float lam;
                         n_pow = power_iteration_warp<M>(R, lane, rl, va, u, pow_ok, lam);
@@ -389,7 +393,8 @@ demod_wide_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         }
                         fb_average_rows<M>(R, ri);
                         bool pow2_ok = false;
-                        n_pow += power_iteration_warp_fb<M>(R, lane, rl, va, v, pow2_ok, trace);
+                        float lam2;
+                        n_pow += power_iteration_warp_fb<M>(R, lane, rl, va, v, pow2_ok, trace, lam2);
                         pow_ok = pow_ok && pow2_ok;
                         v = f2_cx2(cconj(cx2_f2(v)));
                     }

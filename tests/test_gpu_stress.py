@@ -14,6 +14,10 @@ from stress_parity import draw_cases, run_case  # noqa: E402
 # (seed, case index) of every case that failed before the fix
 FAILED = {7: [87, 120, 137, 169, 202, 220, 268], 11: [94, 128, 212, 231, 239], 23: [30, 237]}
 CASES = [(s, k) for s, ks in FAILED.items() for k in ks]
+# row-f4 variants (seed 7): FB in the warp kernel (weak-tone tolerance), spatial smoothing m = 3
+# (order-m power iteration to FP32 noise)
+VARIANT_CASES = [("fb", 120), ("fb", 159), ("fb", 202), ("ss", 11), ("ss", 134), ("ss", 137), ("ss", 187),
+                 ("ss_fb", 100), ("ss_fb", 134)]
 
 
 def _case(seed, idx):
@@ -32,6 +36,15 @@ def test_draw_is_reproducible():
 @pytest.mark.parametrize("seed,idx", CASES)
 def test_stress_regression(seed, idx):
     k = _case(seed, idx)
+    mx, rms, nan, exc = run_case(k)
+    assert nan == 0, k
+    assert rms <= 1e-3 and mx <= 1e-2, (k, mx, rms)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,idx", VARIANT_CASES)
+def test_stress_regression_variant(variant, idx):
+    k = dict(_case(7, idx), variant=variant, subarray=3)
     mx, rms, nan, exc = run_case(k)
     assert nan == 0, k
     assert rms <= 1e-3 and mx <= 1e-2, (k, mx, rms)

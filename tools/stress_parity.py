@@ -38,9 +38,17 @@ def run_case(k):
     """GPU vs oracle on one case; returns (max, rms, nan count, excluded fraction)."""
     w = synth.workload(k["workload"], H=k["H"], W=k["W"], seed=k["wseed"])
     f = synth.make_frame(w, k["t"], snr_db=None if k["snr"] == np.inf else k["snr"])
-    g, _ = bosrm.bos_rootmusic_demod(f.to("cuda"), k["M"])
+    var = k.get("variant", "paper")
+    if var == "paper":
+        g, _ = bosrm.bos_rootmusic_demod(f.to("cuda"), k["M"])
+        o, ofl = R.demod_frame(f.numpy(), k["M"])
+    else:
+        fb = var in ("fb", "ss_fb")
+        m = k.get("subarray", 0) if var.startswith("ss") else 0
+        g, _, _, _ = bosrm.bos_rootmusic_demod_variant(
+            f.to("cuda"), k["M"], variant=bosrm.VARIANT_FB if fb else bosrm.VARIANT_PAPER, subarray_len=m)
+        o, ofl = R.demod_frame(f.numpy(), k["M"], variant="fb" if fb else "paper", subarray_len=m or None)
     torch.cuda.synchronize()
-    o, ofl = R.demod_frame(f.numpy(), k["M"])
     valid = (ofl & R.PARITY_EXCLUDE_MASK) == 0
     e = np.abs(R.wrap(g[0].cpu().numpy().astype(np.float64) - o))[valid]
     nan = int(np.sum(~np.isfinite(e)))
@@ -55,12 +63,17 @@ def main():
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--budget-s", type=float, default=600.0)
+    ap.add_argument("--variant", default="paper", choices=["paper", "fb", "ss", "ss_fb"])
+    ap.add_argument("--subarray", type=int, default=3, help="spatial-smoothing subarray m (ss variants)")
     args = ap.parse_args()
     bad, worst, t0, c = [], 0.0, time.time(), -1
     for k in draw_cases(args.seed, args.cases):
         if time.time() - t0 > args.budget_s:
             break
         c = k["case"]
+        k = dict(k, variant=args.variant, subarray=args.subarray)
+        if args.variant.startswith("ss") and k["M"] <= args.subarray:
+            continue
         mx, rms, nan, exc = run_case(k)
         worst = max(worst, mx)
         if nan or mx > 1e-2 or rms > 1e-3:
