@@ -302,14 +302,10 @@ def estimate_windows(win: np.ndarray, variant: str = "paper", subarray_len: int 
     zy, _, fy = select_root(ry)
     zx, _, fx = select_root(rx)
 
-    # Eq.(15): ω_y = arg z_y, ω_x = -arg z_x (z_x = e^{-jω_x}),
-    # α = ∠ mean(Γ_w e^{-j(ω_x x + ω_y y)}) with local coordinates of the window [R5].
+    # Eq.(15): ω_y = arg z_y, ω_x = -arg z_x (z_x = e^{-jω_x})
     omega_y = np.angle(zy)
     omega_x = -np.angle(zx)
-    o = window_offsets(M).astype(np.float64)
-    phase = omega_x[:, None, None] * o[None, None, :] + omega_y[:, None, None] * o[None, :, None]
-    c = np.mean(win * np.exp(-1j * phase), axis=(1, 2))
-    alpha = np.angle(c)
+    alpha, c = eq15_phase(win, omega_x, omega_y)
 
     flags = np.zeros(N, dtype=np.uint8)
     flags |= np.where(~(fy & fx) | degy | degx, FLAG_NONCONVERGED, 0).astype(np.uint8)
@@ -324,7 +320,84 @@ def estimate_windows(win: np.ndarray, variant: str = "paper", subarray_len: int 
     low = (fro == 0) | (np.abs(c) * M * M < LOW_AMP * M * fro)
     flags |= np.where(low, FLAG_LOW_AMPLITUDE, 0).astype(np.uint8)
     return dict(alpha=alpha, omega_x=omega_x, omega_y=omega_y, flags=flags,
-                z_y=zy, z_x=zx, S=S, margin=marg, c=c)
+                z_y=zy, z_x=zx, S=S, margin=marg, c=c, roots_y=ry, roots_x=rx)
+
+
+def eq15_phase(win: np.ndarray, omega_x, omega_y):
+    """Eq.(15), Algorithm 1 line 11: α = ∠ mean(Γ_w e^{-j(ω_x x + ω_y y)}) with
+    the window's local coordinates (target pixel at the origin, [R5]).  The mean of the
+    demodulated window is the least-squares complex amplitude of the Eq.(3) model for the
+    given (ω_x, ω_y).  Returns (α [N], c [N] complex)."""
+    N, M, _ = win.shape
+    omega_x = np.broadcast_to(np.asarray(omega_x, dtype=np.float64), (N,))
+    omega_y = np.broadcast_to(np.asarray(omega_y, dtype=np.float64), (N,))
+    o = window_offsets(M).astype(np.float64)
+    phase = omega_x[:, None, None] * o[None, None, :] + omega_y[:, None, None] * o[None, :, None]
+    c = np.mean(win * np.exp(-1j * phase), axis=(1, 2))
+    return np.angle(c), c
+
+
+# [R15] Where several outputs are correct (P:L208 leaves the choice between two distinct root
+# pairs equally close to the unit circle open), the valid outputs are the candidates below.
+TAU_CAND = 2.0 * TAU_SEL   # candidate band in |ln|z|| above the closest root (2 × the AMBIGUOUS margin)
+
+
+def root_candidates(roots: np.ndarray, band: float = TAU_CAND):
+    """[R15] For one polynomial's roots [n]: the distinct frequencies among the roots whose
+    distance |ln|z|| to the unit circle is within ``band`` of the closest root (P:L208's
+    candidates when the rule is ambiguous).  Roots whose args differ by ≤ τ_ω are one
+    frequency (the members of a (z, 1/z̄) pair share arg); each frequency is represented by
+    its closest root.  Returns a list of complex roots, closest first."""
+    r = np.asarray(roots)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        d = np.abs(np.log(np.abs(r)))
+    ok = np.isfinite(d)
+    if not ok.any():
+        return []
+    order = np.argsort(np.where(ok, d, np.inf), kind="stable")
+    dmin = d[order[0]]
+    out = []
+    for i in order:
+        if not ok[i] or d[i] > dmin + band:
+            break
+        if all(abs(float(wrap(np.angle(r[i]) - np.angle(q)))) > TAU_OMEGA for q in out):
+            out.append(r[i])
+    return out
+
+
+def candidate_estimates(frame: np.ndarray, py, px, M: int, band: float = TAU_CAND, variant: str = "paper",
+                        subarray_len: int | None = None):
+    """[R15] The set of valid (ω_x, ω_y, α) at each pixel: every combination of the y- and
+    x-axis root candidates (root_candidates) with α from Eq.(15) at that (ω_x, ω_y).  For an
+    unambiguous pixel the set has one member, Algorithm 1's output.  Returns a list (one entry
+    per pixel) of arrays [k, 3]."""
+    py = np.asarray(py, dtype=np.int64).ravel()
+    px = np.asarray(px, dtype=np.int64).ravel()
+    win, _ = extract_windows(np.asarray(frame), py, px, M)
+    res = estimate_windows(win, variant, subarray_len)
+    out = []
+    for p in range(py.size):
+        cy = root_candidates(res["roots_y"][p], band)
+        cx = root_candidates(res["roots_x"][p], band)
+        rows = []
+        for zy in cy:
+            for zx in cx:
+                wy, wx = float(np.angle(zy)), float(-np.angle(zx))
+                a, _ = eq15_phase(win[p:p + 1], wx, wy)
+                rows.append((wx, wy, float(a[0])))
+        out.append(np.array(rows, dtype=np.float64).reshape(-1, 3))
+    return out
+
+
+def eq15_at(frame: np.ndarray, py, px, M: int, omega_x, omega_y):
+    """Eq.(15) at given frequencies for the windows of pixels (py, px) (clamped as in
+    extract_windows): returns (α [N], |c| [N], ‖Γ_w‖_F [N])."""
+    py = np.asarray(py, dtype=np.int64).ravel()
+    px = np.asarray(px, dtype=np.int64).ravel()
+    win, _ = extract_windows(np.asarray(frame), py, px, M)
+    a, c = eq15_phase(win, np.asarray(omega_x, np.float64).ravel(), np.asarray(omega_y, np.float64).ravel())
+    fro = np.sqrt(np.sum(np.abs(win) ** 2, axis=(1, 2)))
+    return a, np.abs(c), fro
 
 
 def default_threads() -> int:

@@ -11,7 +11,7 @@ import torch
 from oracle import rootmusic as R
 from paper_1910_11872_b200 import bosrm, synth
 
-from .parity_util import assert_parity
+from .parity_util import assert_excluded_valid, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -49,9 +49,10 @@ def flag_agreement(g, o):
 def test_f64_ragged_frames(M, fb):
     H, W = (37, 45) if M < 19 else (M + 6, 75)
     f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M), 5, snr_db=10.0)
-    g, gfl = run64(f, M, fb)
+    g, gfl, wx, wy = run64(f, M, fb, omega=True)
     o, ofl = R.demod_frame(f.numpy(), M, variant="fb" if fb else "paper")
-    assert_parity(g, o, ofl, f"FP64 ragged M={M} fb={fb}", rms_tol=RMS64, max_tol=MAX64, max_excluded_frac=0.3)
+    assert_parity(g, o, ofl, f"FP64 ragged M={M} fb={fb}", rms_tol=RMS64, max_tol=MAX64)
+    assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"FP64 ragged M={M} fb={fb}", variant="fb" if fb else "paper")
     assert flag_agreement(gfl, ofl) >= 0.995, (gfl[gfl != ofl], ofl[gfl != ofl])
 
 
@@ -62,7 +63,8 @@ def test_f64_c1_noise_free_full_frame(M):
     f = synth.make_frame(w, 0)
     g, gfl = run64(f, M)
     o, ofl = R.demod_frame(f.numpy(), M)
-    assert_parity(g, o, ofl, f"FP64 C1 M={M}", rms_tol=RMS64, max_tol=MAX64, max_excluded_frac=0.0)
+    s = assert_parity(g, o, ofl, f"FP64 C1 M={M}", rms_tol=RMS64, max_tol=MAX64)
+    assert s["excluded"] == 0, s
     assert flag_agreement(gfl, ofl) >= 0.995
 
 
@@ -122,9 +124,12 @@ def test_f64_spatial_smoothing(M, m, fb):
     H, W = (37, 45) if M < 19 else (M + 6, 75)
     f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=3 * M + m), 5, snr_db=10.0)
     v = bosrm.VARIANT_FP64 | (bosrm.VARIANT_FB if fb else 0)
-    out, fl, _, _ = bosrm.bos_rootmusic_demod_variant(f.to(DEV), M, variant=v, flags=True, subarray_len=m)
+    out, fl, wx, wy = bosrm.bos_rootmusic_demod_variant(f.to(DEV), M, variant=v, flags=True, subarray_len=m,
+                                                        omega=True)
     torch.cuda.synchronize()
     g, gfl = out.cpu().numpy()[0], fl.cpu().numpy()[0]
     o, ofl = R.demod_frame(f.numpy(), M, variant="fb" if fb else "paper", subarray_len=m)
-    assert_parity(g, o, ofl, f"FP64 SS M={M} m={m} fb={fb}", rms_tol=RMS64, max_tol=MAX64, max_excluded_frac=0.3)
+    assert_parity(g, o, ofl, f"FP64 SS M={M} m={m} fb={fb}", rms_tol=RMS64, max_tol=MAX64)
+    assert_excluded_valid(f.numpy(), M, g, wx.cpu().numpy()[0], wy.cpu().numpy()[0], ofl, f"FP64 SS M={M} m={m} fb={fb}",
+                          variant="fb" if fb else "paper", subarray_len=m)
     assert flag_agreement(gfl, ofl) >= 0.995

@@ -10,7 +10,7 @@ import torch
 from oracle import rootmusic as R
 from paper_1910_11872_b200 import bosrm, synth
 
-from .parity_util import assert_parity
+from .parity_util import assert_excluded_valid, assert_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -43,11 +43,13 @@ def test_fb_ragged_frame_parity(M):
     """10 dB fringe frame, ragged sizes; M ≥ 19 frames are wider than one 32-pixel segment."""
     H, W = (37, 45) if M < 19 else (M + 6, 75)
     f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M), 5, snr_db=10.0)
-    g, gfl = run_fb(f, M)
+    g, gfl, wx, wy = run_fb(f, M, omega=True)
     o, ofl = R.demod_frame(f.numpy(), M, variant="fb")
     # FB on these small frames: mostly clamped windows, whose FB R_x is often near-degenerate
-    # ([R13] SMALL_GAP on either axis) — more exclusions than the paper variant
-    assert_parity(g, o, ofl, f"FB ragged M={M}", max_excluded_frac=0.05 if M < 13 else (0.15 if M < 28 else 0.3))
+    # ([R13] SMALL_GAP on either axis): bounded on interior windows, border outputs checked
+    # for validity ([R15])
+    assert_parity(g, o, ofl, f"FB ragged M={M}")
+    assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"FB ragged M={M}", variant="fb")
     assert np.all((gfl & bosrm.FLAG_BORDER) == (ofl & R.FLAG_BORDER))
 
 
@@ -148,9 +150,11 @@ def run_ss(frames_cpu, M, m, fb=False, ref=None, omega=False):
 def test_ss_ragged_frame_parity(M, m, fb):
     H, W = (37, 45) if M < 19 else (M + 6, 75)
     f = synth.make_frame(synth.workload("C3", H=H, W=W, seed=M + m), 5, snr_db=10.0)
-    g, gfl = run_ss(f, M, m, fb)
+    g, gfl, wx, wy = run_ss(f, M, m, fb, omega=True)
     o, ofl = R.demod_frame(f.numpy(), M, variant="fb" if fb else "paper", subarray_len=m)
-    assert_parity(g, o, ofl, f"SS ragged M={M} m={m} fb={fb}", max_excluded_frac=0.3)
+    assert_parity(g, o, ofl, f"SS ragged M={M} m={m} fb={fb}")
+    assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"SS ragged M={M} m={m} fb={fb}",
+                          variant="fb" if fb else "paper", subarray_len=m)
     assert np.all((gfl & bosrm.FLAG_BORDER) == (ofl & R.FLAG_BORDER))
 
 
@@ -175,7 +179,8 @@ def test_ss_noise_free_c1(M, m):
     f = synth.make_frame(w, 0)
     g, gfl = run_ss(f, M, m)
     o, ofl = R.demod_frame(f.numpy(), M, subarray_len=m)
-    assert_parity(g, o, ofl, f"SS C1 M={M} m={m}", max_excluded_frac=0.0)
+    s = assert_parity(g, o, ofl, f"SS C1 M={M} m={m}")
+    assert s["excluded"] == 0, s
 
 
 @pytest.mark.parametrize("M,m", [(8, 3), (12, 3), (20, 7)])
