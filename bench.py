@@ -2,14 +2,23 @@
 """Benchmark: root-MUSIC demod throughput (Mpixel/s, frames/s at 1024²) on N B200s.
 
     python bench.py --gpus N --steps K --warmup W            # CUDA path (libbosrm.so)
+    python bench.py --workload C5 --gpus N ...               # fixed 2048²×2000 stack, strong scaling
     python bench.py --impl reference --gpus N --steps K ...  # FP64 CPU oracle (rank 0 only)
 
-Workload (BASELINE.json configs[2]): C3 — a 1024×1024 time-lapse stack of 100
-frames per rank (local frame 0 = the carrier-only reference, 99 diffusion flow frames),
+Default workload (BASELINE.json configs[2]): C3 — a 1024×1024 time-lapse stack of
+100 frames per rank (local frame 0 = the carrier-only reference, 99 diffusion flow frames),
 window_len 8, model_order 3, SNR 10 dB, generated on the device before timing.  One step =
 the whole hot path over the stack: demodulate the reference (raw α), then all 100 frames
-against it (bos_rootmusic_demod_stack: 2 launches).  Weak scaling: every rank owns 99
-distinct flow frames; value = distinct output pixels of the job / max-over-ranks time.
+against it (2 launches).  Weak scaling: every rank owns 99 distinct flow frames; value =
+distinct output pixels of the job / max-over-ranks time.  This is also what the driver's
+N = 1, 2, 4, 8 scaling run measures.
+
+--workload C5 (configs[4]): ONE 2048²×2000 stack; rank r owns frames [⌊rT/G⌋, ⌊(r+1)T/G⌋)
+(sharding.fixed_stack_indices) plus the reference; strong scaling, value = 2000·2048² / time.
+
+At N = 1 the line also carries ``extra``: the paper's own operating points measured in the
+same run — C2 512² pairs at 0/10/20 dB with M = 11 and M = 8, C3 at M = 15
+(the experiment's L = 7), and the C5 stack on one GPU.
 """
 
 from __future__ import annotations
@@ -42,8 +51,11 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    p.add_argument("--frames", type=int, default=100, help="frames per rank (incl. the reference)")
-    p.add_argument("--size", type=int, default=1024)
+    p.add_argument("--workload", default="C3", choices=["C3", "C5"])
+    p.add_argument("--frames", type=int, default=None, help="C3: frames per rank incl. the reference (100); "
+                   "C5: frames of the whole stack (2000)")
+    p.add_argument("--size", type=int, default=None, help="frame side (C3: 1024, C5: 2048)")
+    p.add_argument("--no-extra", action="store_true", help="skip the N=1 extra operating points")
     p.add_argument("--window-len", type=int, default=8)
     p.add_argument("--ref-mode", default="recompute", choices=["recompute", "broadcast"])
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -163,7 +175,8 @@ def run_reference(args, world, rank):
         return
     from paper_1910_11872_b200 import synth
 
-    w = synth.workload("C3", H=args.size, W=args.size, window_len=args.window_len)
+    size = args.size or (2048 if args.workload == "C5" else 1024)
+    w = synth.workload(args.workload, H=size, W=size, window_len=args.window_len)
     F = args.cpu_sample_frames
     n_px = max(256, args.cpu_sample_px)
     frames = synth.make_stack(w, frames=[0] + list(range(1, F + 1))).numpy()
@@ -176,18 +189,161 @@ def run_reference(args, world, rank):
     per_step = statistics.mean(times)
     outputs = n_px * F
     value = outputs / per_step / 1e6
-    sample = (f"{n_px} random pixels x {F} flow frames of the {args.size}^2 C3 stack per step, plus the same "
-              f"pixels of the reference frame (W={w.window_len})")
+    sample = (f"{n_px} random pixels x {F} flow frames of the {size}^2 {args.workload} stack per step, plus the "
+              f"same pixels of the reference frame (W={w.window_len})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C3 sample: {sample}", "H": args.size, "W": args.size,
+        "config": {"workload": f"{args.workload} sample: {sample}", "H": size, "W": size,
                    "window_len": w.window_len, "model_order": 3},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+WIDE_MIN_M = 21   # first window on the warp-per-pixel kernel (BOS_WIDE_MIN_M, csrc/demod_wide.cuh)
+
+
+def kernel_name(M: int) -> str:
+    return f"bos::{'demod_kernel' if M < WIDE_MIN_M else 'demod_wide_kernel'}<{M},false,false>"
+
+
+def measured_fp32_peak(dev_index: int):
+    """FFMA / FFMA2 / MUFU.RCP peaks of this GPU from tools/microbench (built by build())."""
+    exe = os.path.join(ROOT, "tools", "microbench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        p = subprocess.run([exe, str(dev_index)], capture_output=True, text=True, timeout=120)
+        return json.loads(p.stdout.strip().splitlines()[-1])
+    except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+        return None
+
+
+class StackTimer:
+    """One step = the hot path over a resident stack: raw α of the reference (local frame 0),
+    then every local frame against it (sharding.sharded_stack_step; 2 launches).  Device
+    times with CUDA events on the launching stream, barrier + synchronize around the region,
+    max over ranks."""
+
+    def __init__(self, frames, M, ref_mode, dev):
+        from paper_1910_11872_b200 import bosrm
+        T, H, W = frames.shape
+        self.bosrm, self.frames, self.M, self.ref_mode, self.dev = bosrm, frames, M, ref_mode, dev
+        self.out = torch.empty(T, H, W, dtype=torch.float32, device=dev)
+        self.flags = torch.empty(T, H, W, dtype=torch.uint8, device=dev)
+        self.ref = torch.empty(H, W, dtype=torch.float32, device=dev)
+        self.stream = torch.cuda.current_stream(dev)
+
+    def _raw(self, frame):
+        H, W = frame.shape
+        self.bosrm.bos_rootmusic_demod(frame.unsqueeze(0), self.M, out_phase=self.ref.view(1, H, W))
+        return self.ref
+
+    def step(self, ev=None):
+        from paper_1910_11872_b200 import sharding
+
+        def demod_all(fr, r):
+            if ev is not None:
+                ev[0].record(self.stream)
+            self.bosrm.bos_rootmusic_demod(fr, self.M, ref_phase=r, out_phase=self.out, flags=self.flags)
+            if ev is not None:
+                ev[1].record(self.stream)
+
+        sharding.sharded_stack_step(self.frames, demod_all, self._raw, self.ref_mode, self.ref)
+
+    def run(self, steps, warmup, clocks=None):
+        """→ (max-over-ranks ms for `steps` steps, max-over-ranks mean ms of the T-frame launch, clocks)"""
+        from paper_1910_11872_b200 import sharding
+        for _ in range(warmup):
+            self.step()
+        torch.cuda.synchronize()
+        if sharding.is_dist():
+            dist.barrier()
+        if clocks is not None:
+            clocks.start()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if sharding.is_dist():
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(self.stream)
+        for k in range(steps):
+            self.step(kev[k])
+        t1.record(self.stream)
+        torch.cuda.synchronize()
+        if sharding.is_dist():
+            dist.barrier()
+        ck = clocks.stop() if clocks is not None else None
+        ms = sharding.max_over_ranks(t0.elapsed_time(t1), self.dev)
+        kms = sharding.max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kev), self.dev)
+        return ms, kms, ck
+
+
+def iteration_means(frames, M):
+    from paper_1910_11872_b200 import bosrm
+    cnt = bosrm.bos_rootmusic_iteration_counts(frames, M)
+    npx = max(1, cnt["pixels"])
+    return cnt["power_its"] / npx, cnt["aberth_y"] / npx, cnt["aberth_x"] / npx
+
+
+def extra_points(args, dev):
+    """N = 1 only: the paper's operating points, each timed like the main step (device-resident
+    stack, reference + frames, CUDA events, 2 warm-ups).  Small stacks are repeated so each
+    timed region lasts ≥ 50 ms."""
+    from paper_1910_11872_b200 import synth
+    res = {}
+    c2 = []
+    w2 = synth.workload("C2")
+    for snr in (0.0, 10.0, 20.0):
+        st = synth.make_stack(w2, device=dev, snr_db=snr)
+        for M in (11, 8):
+            tm = StackTimer(st, M, "recompute", dev)
+            ms, kms, _ = tm.run(50, 3)
+            px = 2 * 512 * 512 * 50
+            k = iteration_means(st[1:], M)
+            c2.append({"snr_db": snr, "window_len": M, "mpix_s": px / (ms / 1e3) / 1e6,
+                       "iters": {"power": k[0], "aberth_y": k[1], "aberth_x": k[2]},
+                       "flops_per_px": flops_per_pixel(M, *k)})
+            del tm
+        del st
+    res["c2_pair_512"] = {"what": "512^2 reference + flow pair (C2), per-step = raw ref + 2-frame stack, 50 steps",
+                          "points": c2}
+    for snr in (0.0, 10.0, 20.0):
+        r0 = next(p for p in c2 if p["snr_db"] == snr and p["window_len"] == 11)
+        r10 = next(p for p in c2 if p["snr_db"] == 10.0 and p["window_len"] == 11)
+        res["c2_pair_512"][f"m11_{int(snr)}db_vs_10db"] = r0["mpix_s"] / r10["mpix_s"]
+    # C3 at the experiment's window (L = 7 → M = 15, P:L389)
+    w3 = synth.workload("C3", window_len=15)
+    st = synth.make_stack(w3, device=dev)
+    tm = StackTimer(st, 15, "recompute", dev)
+    ms, kms, _ = tm.run(3, 2)
+    k = iteration_means(st[1:5], 15)
+    f = flops_per_pixel(15, *k)
+    res["c3_m15"] = {"mpix_s": 100 * 1024 * 1024 * 3 / (ms / 1e3) / 1e6, "kernel": kernel_name(15),
+                     "frac_own_model": f * 100 * 1024 * 1024 / (kms / 1e3) / 1e12 / nominal_peak(),
+                     "iters": {"power": k[0], "aberth_y": k[1], "aberth_x": k[2]}}
+    del tm, st
+    torch.cuda.empty_cache()
+    # C5 on one GPU: the whole fixed 2048²×2000 stack, one step (≈ 8.4e9 pixels)
+    w5 = synth.workload("C5")
+    st = torch.empty(w5.T, w5.H, w5.W, dtype=torch.complex64, device=dev)
+    synth.make_stack(w5, device=dev, out=st)
+    tm = StackTimer(st, 8, "recompute", dev)
+    ms, kms, _ = tm.run(1, 1)
+    res["c5_n1"] = {"frames": w5.T, "H": w5.H, "W": w5.W, "window_len": 8, "step_ms": ms,
+                    "mpix_s": w5.T * w5.H * w5.W / (ms / 1e3) / 1e6, "kernel_ms": kms}
+    del tm, st
+    torch.cuda.empty_cache()
+    return res
+
+
+def nominal_peak(sm_mhz: float | None = None) -> float:
+    """FP32 FMA peak, TFLOP/s: 148 SM × 128 lanes × 2 flop × the max SM clock (MEASURED_PEAKS)."""
+    f = sm_mhz if sm_mhz is not None else float(peaks().get("sm_max_mhz", 1965.0))
+    return B200_SMS * FP32_LANES_PER_SM * 2 * f * 1e6 / 1e12
 
 
 def run_cuda(args, world, rank, local):
@@ -199,82 +355,44 @@ def run_cuda(args, world, rank, local):
     torch.cuda.set_device(dev)
     bosrm.lib()
     M = args.window_len
-    T = args.frames
-    w = synth.workload("C3", H=args.size, W=args.size, window_len=M)
-    H = W = args.size
+    c5 = args.workload == "C5"
+    size = args.size or (2048 if c5 else 1024)
+    H = W = size
     plane = H * W
-    gidx = sharding.rank_frame_indices(rank, world, T)
+    if c5:
+        T_job = args.frames or 2000
+        w = synth.workload("C5", H=H, W=W, window_len=M, T=T_job)
+        gidx = sharding.fixed_stack_indices(rank, world, T_job)
+        out_frames = T_job
+        scaling = "strong"
+    else:
+        T_rank = args.frames or 100
+        w = synth.workload("C3", H=H, W=W, window_len=M)
+        gidx = sharding.rank_frame_indices(rank, world, T_rank)
+        out_frames = sharding.distinct_output_frames(world, T_rank)
+        scaling = "weak"
+    T = len(gidx)
     frames = torch.empty(T, H, W, dtype=torch.complex64, device=dev)
     synth.make_stack(w, frames=gidx, device=dev, out=frames)
-    out = torch.empty(T, H, W, dtype=torch.float32, device=dev)
-    flags = torch.empty(T, H, W, dtype=torch.uint8, device=dev)
-    ref = torch.empty(H, W, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
-
-    stream = torch.cuda.current_stream()
-    k_start = torch.cuda.Event(enable_timing=True)
-    k_end = torch.cuda.Event(enable_timing=True)
-    kernel_ms = []
-
-    def demod_raw(frame):
-        bosrm.bos_rootmusic_demod(frame.unsqueeze(0), M, out_phase=ref.view(1, H, W))
-        return ref
-
-    def demod_all(fr, r, timed=False):
-        if timed:
-            k_start.record(stream)
-        bosrm.bos_rootmusic_demod(fr, M, ref_phase=r, out_phase=out, flags=flags)
-        if timed:
-            k_end.record(stream)
-
-    def step(timed=False):
-        sharding.sharded_stack_step(frames, lambda fr, r: demod_all(fr, r, timed), demod_raw, args.ref_mode, ref)
 
     # iteration counts for the algorithmic flop model (outside the timed region)
-    cnt = bosrm.bos_rootmusic_iteration_counts(frames[1:min(T, 5)], M)
-    npx = max(1, cnt["pixels"])
-    k_pi, k_aby, k_abx = cnt["power_its"] / npx, cnt["aberth_y"] / npx, cnt["aberth_x"] / npx
-    del cnt
+    k_pi, k_aby, k_abx = iteration_means(frames[1:min(T, 5)], M)
+    mb = measured_fp32_peak(dev.index) if rank == 0 else None
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if sharding.is_dist():
-        dist.barrier()
-    sampler = ClockSampler(dev.index)
-    sampler.start()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if sharding.is_dist():
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_start.record(stream)
-    for _ in range(args.steps):
-        step(timed=True)
-        kernel_ms.append((k_start, k_end))
-        k_start = torch.cuda.Event(enable_timing=True)
-        k_end = torch.cuda.Event(enable_timing=True)
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    if sharding.is_dist():
-        dist.barrier()
-    clocks = sampler.stop()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    kern = [a.elapsed_time(b) for a, b in kernel_ms]
-    elapsed_ms = sharding.max_over_ranks(elapsed_ms, dev)
-    kern_ms = sharding.max_over_ranks(statistics.mean(kern), dev)
+    tm = StackTimer(frames, M, args.ref_mode, dev)
+    elapsed_ms, kern_ms, clocks = tm.run(args.steps, args.warmup, ClockSampler(dev.index))
+    out, flags = tm.out, tm.flags
 
-    out_frames = sharding.distinct_output_frames(world, T)
     units = out_frames * plane * args.steps
     value = units / (elapsed_ms / 1e3) / 1e6
     ms_per_step = elapsed_ms / args.steps
 
-    # roofline of the dominant kernel (the T-frame demod launch; ref launch is 1/T of it)
-    P = peaks()
+    # roofline of the dominant kernel (the T-frame demod launch; the ref launch is 1/T of it)
     f_px = flops_per_pixel(M, k_pi, k_aby, k_abx)
     achieved = f_px * T * plane / (kern_ms / 1e3) / 1e12
-    sm_max = float(P.get("sm_max_mhz", 1965.0))
-    peak = B200_SMS * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    sm_max = float(peaks().get("sm_max_mhz", 1965.0))
+    peak = nominal_peak(sm_max)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
@@ -284,17 +402,22 @@ def run_cuda(args, world, rank, local):
     except (OSError, ValueError, KeyError):
         traffic = None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/)", "kernel": f"bos::{'demod_kernel' if M <= 18 else 'demod_wide_kernel'}<{M},false,false>", "kernel_ms": kern_ms,
-                "kernel_share_of_step": kern_ms / ms_per_step,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/)",
+                "kernel": kernel_name(M), "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms_per_step,
                 "flops_per_px": f_px, "iters": {"power": k_pi, "aberth_y": k_aby, "aberth_x": k_abx},
-                "peak_basis": f"FP32 FMA: {B200_SMS} SM x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz",
+                "peak_basis": f"nominal FP32 FMA (the contract): {B200_SMS} SM x {FP32_LANES_PER_SM} lanes x 2 x "
+                              f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                 "hbm_gbs": (T * plane * 13 + plane * 8) / (kern_ms / 1e3) / 1e9}
+    if mb and mb.get("ffma_tflops"):
+        roofline["peak_measured_ffma"] = mb["ffma_tflops"]
+        roofline["frac_vs_measured_ffma"] = achieved / mb["ffma_tflops"]
+        roofline["microbench"] = mb
     if clocks and clocks.get("sm_mhz"):
-        roofline["frac_at_measured_clock"] = achieved / (B200_SMS * FP32_LANES_PER_SM * 2 * clocks["sm_mhz"] / 1e6)
+        roofline["frac_at_measured_clock"] = achieved / nominal_peak(clocks["sm_mhz"])
 
     # e2e: the same step through the C-ABI host-buffer entry point (H2D/D2H in the region)
     e2e = None
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5 if not c5 else 1))
     if e2e_steps > 0:
         h_frames = frames.cpu().pin_memory()
         h_out = torch.empty(T, H, W, dtype=torch.float32).pin_memory()
@@ -312,6 +435,7 @@ def run_cuda(args, world, rank, local):
             dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
+        stream = torch.cuda.current_stream(dev)
         a.record(stream)
         for _ in range(e2e_steps):
             e2e_step()
@@ -335,34 +459,48 @@ def run_cuda(args, world, rank, local):
         o, ofl, pix, dt, threads = oracle_sample(host, M, args.cpu_sample_px, seed=1)
         n_out = args.cpu_sample_px * F
         cpu_val = n_out / dt / 1e6
-        sample = (f"{args.cpu_sample_px} random pixels x {F} flow frames of this C3 stack, plus the same pixels of "
-                  f"the reference frame ({dt:.1f} s wall)")
+        sample = (f"{args.cpu_sample_px} random pixels x {F} flow frames of this {args.workload} stack, plus the same "
+                  f"pixels of the reference frame ({dt:.1f} s wall)")
         cpu_baseline = {"value": cpu_val, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
         # parity of the timed GPU output at the same pixels (north_star tolerance)
         from oracle import rootmusic as R
         g = out[1:F + 1].cpu().numpy()[:, pix[0], pix[1]]
         valid = (ofl & R.PARITY_EXCLUDE_MASK) == 0
         e = R.wrap(g - o)[valid]
-        e = e[np.isfinite(e)]
+        gpu_nan = int(np.sum(~np.isfinite(e)))          # NaN on an oracle-valid pixel is a failure
+        ef = e[np.isfinite(e)]
         gfl = flags[1:F + 1].cpu().numpy()[:, pix[0], pix[1]]
         gpu_only = ((gfl & R.PARITY_EXCLUDE_MASK) != 0) & valid     # flagged by the GPU, not the oracle
-        parity = {"rms": float(math.sqrt(np.mean(e * e))), "max": float(np.max(np.abs(e))), "n": int(e.size),
+        parity = {"rms": float(math.sqrt(np.mean(ef * ef))) if ef.size else None,
+                  "max": float(np.max(np.abs(ef))) if ef.size else None, "n": int(e.size), "gpu_nan": gpu_nan,
                   "excluded_frac": float(1 - valid.mean()), "gpu_only_flagged_frac": float(gpu_only.mean()),
                   "tol": {"rms": 1e-3, "max": 1e-2}}
 
+    del tm, frames, out, flags
+    torch.cuda.empty_cache()
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra and not c5:
+        extra = extra_points(args, dev)
+
     if rank == 0:
+        if c5:
+            wl = (f"C5: one {H}x{W} stack of {out_frames} frames (frame 0 = carrier-only reference, diffusion flow "
+                  f"frames), frames [floor(rT/G), floor((r+1)T/G)) + the reference on rank r, window_len {M}, "
+                  f"model_order 3, SNR 10 dB")
+        else:
+            wl = (f"C3: {H}x{W} time-lapse stack, {T} frames/rank (reference + {T - 1} diffusion flow frames), "
+                  f"window_len {M}, model_order 3, SNR 10 dB")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "frames_per_s_1024": value / 1.048576 * (1024 * 1024 / plane) if plane else None,
-            "config": {"workload": f"C3: {H}x{W} time-lapse stack, {T} frames/rank (reference + {T - 1} diffusion "
-                                   f"flow frames), window_len {M}, model_order 3, SNR 10 dB",
-                       "H": H, "W": W, "frames_per_rank": T, "window_len": M, "model_order": 3,
+            "frames_per_s_1024": value / 1.048576,
+            "config": {"workload": wl, "H": H, "W": W, "frames_per_rank": T, "window_len": M, "model_order": 3,
                        "ref_mode": args.ref_mode, "distinct_output_frames": out_frames,
                        "l2": f"inputs {T * plane * 8 / 2**20:.0f} MiB/rank > 126 MB L2 (no flush needed)"},
             "gpu_launches": 2 * args.steps,
             "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "clocks": clocks, "parity": parity,
+            "extra": extra,
         }
         if cpu_baseline:
             line["speedup_vs_cpu_oracle"] = value / cpu_baseline["value"]

@@ -70,6 +70,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
     if not force and os.path.exists(lib) and os.path.exists(stamp):
         with open(stamp) as fh:
             if fh.read().strip() == digest:
+                if out is None and not os.path.exists(MICROBENCH):
+                    build_microbench()
                 return lib
     cc = nvcc()
     jobs = jobs or max(1, min(len(WINDOW_LENS) + 1, os.cpu_count() or 1))
@@ -101,9 +103,23 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, d
     _run([cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-L" + cudalib, "-lcufft",
           "-Xlinker", "-rpath=" + cudalib], os.path.join(build_dir, "link.log"))
     os.replace(tmp, lib)
+    if out is None:
+        build_microbench(cc)
     with open(stamp, "w") as fh:
         fh.write(digest)
     return lib
+
+
+MICROBENCH_SRC = os.path.join(ROOT, "tools", "microbench.cu")
+MICROBENCH = os.path.join(ROOT, "tools", "microbench")
+
+
+def build_microbench(cc: str | None = None) -> str:
+    """The FP32-pipe microbenchmark (FFMA / FFMA2 / MUFU.RCP peaks, tools/microbench.cu) whose
+    FFMA figure bench.py reports as the measured roofline denominator beside the nominal one."""
+    cc = cc or nvcc()
+    _run([cc, *ARCH, "-O3", "-o", MICROBENCH, MICROBENCH_SRC], os.path.join(BUILD, "microbench.log"))
+    return MICROBENCH
 
 
 if __name__ == "__main__":

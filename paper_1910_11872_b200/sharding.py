@@ -30,6 +30,17 @@ def rank_frame_indices(rank: int, world: int, T: int) -> list[int]:
     return [0] + list(range(rank * (T - 1) + 1, (rank + 1) * (T - 1) + 1))
 
 
+def fixed_stack_indices(rank: int, world: int, T: int) -> list[int]:
+    """Strong scaling of ONE fixed T-frame stack (C5): rank r owns the global
+    frames [⌊rT/G⌋, ⌊(r+1)T/G⌋); its local stack is the reference (global frame 0) followed by
+    its own frames other than 0 (rank 0's range starts with the reference itself, whose output
+    is φ_ref − φ_ref = 0 and is written by the raw reference demod's difference anyway)."""
+    if T < 2 or not 0 <= rank < world:
+        raise ValueError("need T >= 2 and 0 <= rank < world")
+    lo, hi = rank * T // world, (rank + 1) * T // world
+    return [0] + [t for t in range(lo, hi) if t != 0]
+
+
 def distinct_output_frames(world: int, T: int) -> int:
     """Distinct output frames of the whole job: the reference plus every rank's flow frames."""
     return world * (T - 1) + 1

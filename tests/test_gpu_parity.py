@@ -258,8 +258,12 @@ def test_low_snr_excluded_pixels_valid(M):
 def test_exact_two_tone_tie_frame(M):
     """Every interior window is an exact two-frequency tie (tests/test_oracle_ambiguous.py:
     column vector e^{jw0 y}·(real) ⇒ conjugate-symmetric roots about w0): P:L208's "closest
-    root" is not unique.  The oracle flags AMBIGUOUS; the GPU must flag it too and return
-    one of the two valid answers ([R15])."""
+    root" is not unique wherever the closest root is one of the conjugate pairs.  (The
+    polynomial in w = z·e^{-j w0} has real coefficients, so a root may also sit on the real
+    axis, angle w0 or w0+π, and be unique: at M = 5 that happens on 4 of the 13 interior rows,
+    where the column's 2cos(δ(py+o)) profile changes sign inside the window.)  The oracle
+    flags AMBIGUOUS; the GPU must flag it too and return one of the valid answers ([R15]);
+    the rows with a unique closest root are ordinary parity pixels."""
     w0, delta = 0.5, 0.6 if M < 11 else 0.45
     H, W = M + 12, 70
     y, x = np.mgrid[0:H, 0:W]
@@ -268,10 +272,13 @@ def test_exact_two_tone_tie_frame(M):
     g, gfl, wx, wy = run_gpu_ex(f, M)
     o, ofl = R.demod_frame(f.numpy(), M)
     interior = (ofl & R.FLAG_BORDER) == 0
-    assert np.all(ofl[interior] & R.FLAG_AMBIGUOUS)
-    assert np.mean((gfl[interior] & bosrm.FLAG_AMBIGUOUS) != 0) >= 0.99
+    amb = interior & ((ofl & R.FLAG_AMBIGUOUS) != 0)
+    assert amb.sum() >= 0.6 * interior.sum()
+    assert np.mean((gfl[amb] & bosrm.FLAG_AMBIGUOUS) != 0) >= 0.99
+    # the tie frame is flagged by construction: no interior-fraction bound, parity elsewhere
+    assert_parity(g, o, ofl, f"tie M={M}", max_interior_excluded_frac=1.0)
     st = assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"tie M={M}")
-    assert st["ambiguous"] >= int(interior.sum())
+    assert st["ambiguous"] >= int(amb.sum())
 
 
 @pytest.mark.parametrize("M", [17, 20, 21, 25])

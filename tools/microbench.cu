@@ -3,6 +3,7 @@
 // independent chains per thread, timed with CUDA events.  Prints one JSON line.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench tools/microbench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int kChains = 8;
@@ -84,11 +85,13 @@ float time_ms(F launch) {
     return best;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const int dev = argc > 1 ? atoi(argv[1]) : 0;
+    cudaSetDevice(dev);
     cudaDeviceProp p;
-    cudaGetDeviceProperties(&p, 0);
+    cudaGetDeviceProperties(&p, dev);
     int clk_khz = 0;
-    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
     float* out;
     cudaMalloc(&out, 1024 * sizeof(float));
     const int blocks = p.multiProcessorCount * 8, threads = 256;
