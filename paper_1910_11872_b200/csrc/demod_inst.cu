@@ -1,10 +1,13 @@
 // demod_inst.cu — explicit instantiation of the demod kernel launcher for one window size
 // M = BOS_INST_M (the build compiles this file once per M, in parallel).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "demod_f64.cuh"
 #include "demod_kernel.cuh"
 #include "demod_ss.cuh"
+#include "demod_strip.cuh"
 #include "demod_wide.cuh"
 #include "launch.h"
 
@@ -14,11 +17,68 @@
 
 namespace bos {
 
+// BOS_THREAD_KERNEL=row / =strip forces that kernel on the paper path for M ≤ BOS_STRIP_MAX_M
+// (A/B timing and the bitwise test, tests/test_gpu_strip.py); unset = by launch size.  Read per
+// launch: a plain getenv.  0 = auto, 1 = row, 2 = strip.
+inline int thread_kernel_forced() {
+    const char* e = std::getenv("BOS_THREAD_KERNEL");
+    if (e == nullptr) return 0;
+    return std::strcmp(e, "row") == 0 ? 1 : (std::strcmp(e, "strip") == 0 ? 2 : 0);
+}
+
+// Strip kernel launch: one work item (S rows × 32 columns of one frame) per warp (demod_strip.cuh).
+// Launches too small for S ≥ BOS_STRIP_MIN_ROWS at ≥ 4 items per resident warp return
+// cudaErrorNotReady without launching (a cold start per 2–4 rows costs more than the sliding
+// covariance saves: C2 512² pairs ran 9 % slower) and go to the row kernel.
+template <int M, bool COUNT>
+cudaError_t launch_strip(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
+                         uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
+                         cudaStream_t s) {
+    constexpr int WARPS = strip_warps<M>();
+    constexpr size_t smem = strip_smem_bytes<M>();
+    auto kern = demod_strip_kernel<M, COUNT>;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static int cached[64][2];                  // per device: CTAs/SM, SMs (benign racy cache)
+    int nb = (dev >= 0 && dev < 64) ? cached[dev][0] : 0, sms = (dev >= 0 && dev < 64) ? cached[dev][1] : 0;
+    if (nb <= 0 || sms <= 0) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, WARPS * 32, smem);
+        if (e != cudaSuccess) return e;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        if (nb < 1) return cudaErrorInvalidConfiguration;
+        if (dev >= 0 && dev < 64) { cached[dev][0] = nb; cached[dev][1] = sms; }
+    }
+    const long long nbx = (W + kBX - 1) / kBX;
+    const long long resident = (long long)nb * sms * WARPS;
+    const long long row_items = (long long)n_frames * H * nbx;    // (frame, row, 32-column block)
+    // S rows per item; small launches use shorter strips so every resident warp gets ≥ 4 items
+    int S = BOS_STRIP_ROWS;
+    while (S > 2 && row_items / S < 4 * resident) S >>= 1;
+    if (S < BOS_STRIP_MIN_ROWS && thread_kernel_forced() != 2)
+        return cudaErrorNotReady;                                   // too small: the caller uses the row kernel
+    const long long items = (long long)n_frames * ((H + S - 1) / S) * nbx;
+    const long long grid = std::min<long long>((items + WARPS - 1) / WARPS, 0x7fffffffLL);
+    kern<<<(unsigned)grid, WARPS * 32, smem, s>>>(frames, n_frames, H, W, S, ref, out, flags, omega_x, omega_y,
+                                                  counters);
+    return cudaGetLastError();
+}
+
 template <int M, bool COUNT, bool FB>
 cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
     const dim3 block(kBX, kBY, 1);
+    if constexpr (!FB && !COUNT && M <= kStripMaxM) {   // paper path: sliding-covariance strip kernel
+        if (thread_kernel_forced() != 1) {
+            const cudaError_t e =
+                launch_strip<M, false>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters, s);
+            if (e != cudaErrorNotReady) return e;
+        }
+    }
     if constexpr (M >= wide_min_m<FB>()) {
         const dim3 grid((unsigned)((W + kBX - 1) / kBX), (unsigned)((H + kBY - 1) / kBY),
                         (unsigned)std::min(n_frames, 65535));

@@ -120,7 +120,7 @@ constexpr float kLowSnrRatio = BOS_LOWSNR_RATIO;
 #endif
 constexpr float kWeakNewtonRatio = BOS_WEAK_NEWTON_RATIO;
 #ifndef BOS_WEAK_MODE
-#define BOS_WEAK_MODE 1     // 1: weak pixels start from kAberthLowSnrTol2; 0: per-pixel Newton-ratio stop
+#define BOS_WEAK_MODE 0     // 1: weak pixels start from kAberthLowSnrTol2; 0: per-pixel Newton-ratio stop
 #endif
 constexpr float kAberthLowSnrTol2 = 1e-4f;
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
@@ -650,6 +650,153 @@ __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const 
     return n;
 }
 
+// a3, second singular vector side: v_1 = Γ_w^H u_1 / ‖Γ_w^H u_1‖ (the SVD identity)
+template <int M, int TW>
+__device__ __forceinline__ void v1_from_window(const float2* win, const cx2 (&u)[M], float2 (&v)[M]) {
+    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+    // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
+    cx2 unj[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) unj[i] = mul2(cx2_make(cx2_im(u[i]), cx2_re(u[i])), kPosNeg);
+    cx2 vp[M];
+    float vn = 0.0f;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        cx2 acc = 0ull;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float2 g = win[i * TW + k];
+            acc = fma2(cx2_bcast(g.x), u[i], fma2(cx2_bcast(g.y), unj[i], acc));
+        }
+        vp[k] = acc;
+        vn += cabs2(cx2_f2(acc));
+    }
+    const cx2 vinv = cx2_bcast(rsqrtf(vn));
+#pragma unroll
+    for (int k = 0; k < M; ++k) v[k] = cx2_f2(mul2(vp[k], vinv));
+}
+
+// a4 + a5 (both axes) and a6 for one pixel, shared by the row kernel (demod_kernel) and the
+// strip kernel (demod_strip.cuh): music_coeffs → symmetric Aberth from the rotated template →
+// selection + polish (+ safety nets) → Eq.(15) least-squares phase.  Sets NONCONVERGED,
+// AMBIGUOUS and LOW_AMPLITUDE in fl; returns the raw α (before the reference difference) and
+// the selected roots zx (x axis, from v_1) and zy (y axis, from u_1).
+template <int M, int TW, bool FB>
+__device__ __forceinline__ float roots_and_phase(const float2* win, const cx2 (&u)[M], const float2 (&v)[M], float trace,
+                                                 bool pow_ok, uint8_t& fl, int& n_aby, int& n_abx, float2& zx_out,
+                                                 float2& zy_out) {
+    constexpr int N = 2 * M - 2;
+    constexpr int O0 = (M - 1) / 2;
+    float2 uf[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) uf[i] = cx2_f2(u[i]);
+
+    // ---- a4 + a5, y axis (u_1) then x axis (v_1), one rolled loop ----
+    float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
+    float my = CUDART_INF_F, mx = CUDART_INF_F;
+    bool aby_ok = false, abx_ok = false;
+#pragma unroll 1
+    for (int axis = 0; axis < 2; ++axis) {
+        float2 q[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : uf[i];
+        cx2 c[N + 1];
+        const float2 rot = music_coeffs<M>(q, c);
+        cx2 z[N / 2];       // the inside half of the rotated template
+#pragma unroll
+        for (int j = 0; j < N / 2; ++j) z[j] = f2_cx2(cmul(kTemplateRoots[bos_template_offset(M) + j], rot));
+        bool ok = false;
+        int its = 0;
+        float marg = CUDART_INF_F;
+        float2 zs, z2;
+        float tol2 = (BOS_WEAK_MODE == 1 && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
+#pragma unroll 1
+        for (int attempt = 0;; ++attempt) {
+            its += aberth_sym<N, newton_stop<FB, M>()>(c, z, ok, tol2, BOS_WEAK_MODE == 0 && (fl & kFlagWeakInternal));
+            zs = select_root<N / 2>(z, marg, z2);
+            // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
+            // ~1e-5 there); Newton steps on the selected root alone then make it
+            // FP32-accurate (quadratic) at 1/(M−1) of a sweep each.
+            const float2 zsel = zs;
+#pragma unroll 1
+            for (int t = 0; t < kPolishMax; ++t) {
+                const float2 w = polish_step<N>(c, zs);
+                const float w2 = cabs2(w);
+                if (w2 < 1e30f) zs = csub(zs, w);
+                if (polish_done(t, w2)) break;
+            }
+            // Loose sweeps can park an approximation between roots; polished, it lands on
+            // a root that is no longer the closest (or moves far).  Then converge all
+            // roots tightly and select again.  (Near-double roots legitimately move
+            // ~0.02 toward the circle during the polish: that is not a fallback.)
+            const float dsel = ln_dist(zs), dsec = ln_dist(z2) - 1e-3f;
+            if (attempt == 0 && (!(dsel <= dsec || marg == CUDART_INF_F) ||
+                                 !(cabs2(csub(zs, zsel)) <= kMoved2))) {
+                tol2 = kAberthTightTol2;
+                continue;
+            }
+            break;
+        }
+        // Near-tie between two frequencies: the loose sweeps may rank them wrongly, so
+        // polish the runner-up too and re-select between the two converged roots.
+        if (marg < kRefineMargin) {
+#pragma unroll 1
+            for (int t = 0; t < kPolishMax; ++t) {
+                const float2 w = polish_step<N>(c, z2);
+                const float w2 = cabs2(w);
+                if (w2 < 1e30f) z2 = csub(z2, w);
+                if (polish_done(t, w2)) break;
+            }
+            const float d1 = ln_dist(zs), d2 = ln_dist(z2);
+            if (d2 < d1) zs = z2;
+            marg = fabsf(d2 - d1);
+        }
+        if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
+        else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }
+    }
+    if (!pow_ok || !aby_ok || !abx_ok || !isfinite(zy.x + zy.y + zx.x + zx.y))
+        fl |= kFlagNonconverged;
+    if (fminf(my, mx) < kTauSel) fl |= kFlagAmbiguous;
+
+    // ---- a6: Eq.(15) least-squares phase at the target pixel ----
+    // ẑ_x = e^{-jω_x}, ẑ_y = e^{jω_y}; basis e^{-j(ω_x o_k + ω_y o_i)} = ẑ_x^{o_k} conj(ẑ_y)^{o_i}
+    const float2 hx = cscale(zx, rsqrtf(cabs2(zx)));
+    const float2 hy = cscale(zy, rsqrtf(cabs2(zy)));
+    // row_i = Σ_k Γ(i,k)·tw_k = Σ_k re(g)·tw_k + im(g)·(j·tw_k)  (two FFMA2 per sample)
+    cx2 tw[M], twj[M];
+    {
+        float2 p = make_float2(1.0f, 0.0f);
+#pragma unroll
+        for (int k = 0; k < O0; ++k) p = cmul(p, cconj(hx));
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            tw[k] = cx2_make(p.x, p.y);
+            twj[k] = cx2_make(-p.y, p.x);
+            p = cmul(p, hx);
+        }
+    }
+    float2 q = make_float2(1.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i < O0; ++i) q = cmul(q, hy);
+    float2 csum = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+    for (int i = 0; i < M; ++i) {
+        cx2 row = 0ull;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            const float2 g = win[i * TW + k];
+            row = fma2(cx2_bcast(g.x), tw[k], fma2(cx2_bcast(g.y), twj[k], row));
+        }
+        csum = cfma(cx2_f2(row), q, csum);
+        q = cmul(q, cconj(hy));
+    }
+    if (!(cabs2(csum) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
+    float a = atan2f(csum.y, csum.x);
+    zx_out = zx;
+    zy_out = zy;
+    return a;
+}
+
 // CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).
 // (measured per M on C4: 4 CTAs/SM up to M = 9, 3 for M = 10, 11, 2 for 12, 13 — one more CTA
 // costs 4–27 % at M = 10, 12, 13 through spills, one fewer is slower everywhere)
@@ -861,26 +1008,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     if constexpr (!newton_stop<FB, M>())   // weak-tone window (see newton_stop); a flag bit, not a register
                         if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
                     }
-                    // v_1 ∝ Γ_w^H u_1:  v_k = Σ_i conj(Γ(i,k)) u_i = Σ_i re(g)·u_i + im(g)·(−j·u_i)
-                    cx2 unj[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) unj[i] = mul2(cx2_make(cx2_im(u[i]), cx2_re(u[i])), kPosNeg);
-                    cx2 vp[M];
-                    float vn = 0.0f;
-#pragma unroll
-                    for (int k = 0; k < M; ++k) {
-                        cx2 acc = 0ull;
-#pragma unroll
-                        for (int i = 0; i < M; ++i) {
-                            const float2 g = win[i * TW + k];
-                            acc = fma2(cx2_bcast(g.x), u[i], fma2(cx2_bcast(g.y), unj[i], acc));
-                        }
-                        vp[k] = acc;
-                        vn += cabs2(cx2_f2(acc));
-                    }
-                    const cx2 vinv = cx2_bcast(rsqrtf(vn));
-#pragma unroll
-                    for (int k = 0; k < M; ++k) v[k] = cx2_f2(mul2(vp[k], vinv));
+                    v1_from_window<M, TW>(win, u, v);
                 } else {
                     // variant f4 (not in the paper): dominant eigenvectors of the FB-averaged
                     // R_y and of FB(S), S = Σ_i row_i row_i^H = conj(R_x); v_1 = conj(eigvec of FB(S))
@@ -895,111 +1023,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
 #pragma unroll
                     for (int k = 0; k < M; ++k) v[k] = cconj(cx2_f2(sv[k]));
                 }
-                float2 uf[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) uf[i] = cx2_f2(u[i]);
-
-                // ---- a4 + a5, y axis (u_1) then x axis (v_1), one rolled loop ----
-                float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
-                float my = CUDART_INF_F, mx = CUDART_INF_F;
-                bool aby_ok = false, abx_ok = false;
-#pragma unroll 1
-                for (int axis = 0; axis < 2; ++axis) {
-                    float2 q[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) q[i] = axis ? v[i] : uf[i];
-                    cx2 c[N + 1];
-                    const float2 rot = music_coeffs<M>(q, c);
-                    cx2 z[N / 2];       // the inside half of the rotated template
-#pragma unroll
-                    for (int j = 0; j < N / 2; ++j) z[j] = f2_cx2(cmul(kTemplateRoots[bos_template_offset(M) + j], rot));
-                    bool ok = false;
-                    int its = 0;
-                    float marg = CUDART_INF_F;
-                    float2 zs, z2;
-                    float tol2 = (BOS_WEAK_MODE == 1 && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
-#pragma unroll 1
-                    for (int attempt = 0;; ++attempt) {
-                        its += aberth_sym<N, newton_stop<FB, M>()>(c, z, ok, tol2, BOS_WEAK_MODE == 0 && (fl & kFlagWeakInternal));
-                        zs = select_root<N / 2>(z, marg, z2);
-                        // The sweeps stop once every root moved < 0.032 (cubic convergence leaves
-                        // ~1e-5 there); Newton steps on the selected root alone then make it
-                        // FP32-accurate (quadratic) at 1/(M−1) of a sweep each.
-                        const float2 zsel = zs;
-#pragma unroll 1
-                        for (int t = 0; t < kPolishMax; ++t) {
-                            const float2 w = polish_step<N>(c, zs);
-                            const float w2 = cabs2(w);
-                            if (w2 < 1e30f) zs = csub(zs, w);
-                            if (polish_done(t, w2)) break;
-                        }
-                        // Loose sweeps can park an approximation between roots; polished, it lands on
-                        // a root that is no longer the closest (or moves far).  Then converge all
-                        // roots tightly and select again.  (Near-double roots legitimately move
-                        // ~0.02 toward the circle during the polish: that is not a fallback.)
-                        const float dsel = ln_dist(zs), dsec = ln_dist(z2) - 1e-3f;
-                        if (attempt == 0 && (!(dsel <= dsec || marg == CUDART_INF_F) ||
-                                             !(cabs2(csub(zs, zsel)) <= kMoved2))) {
-                            tol2 = kAberthTightTol2;
-                            continue;
-                        }
-                        break;
-                    }
-                    // Near-tie between two frequencies: the loose sweeps may rank them wrongly, so
-                    // polish the runner-up too and re-select between the two converged roots.
-                    if (marg < kRefineMargin) {
-#pragma unroll 1
-                        for (int t = 0; t < kPolishMax; ++t) {
-                            const float2 w = polish_step<N>(c, z2);
-                            const float w2 = cabs2(w);
-                            if (w2 < 1e30f) z2 = csub(z2, w);
-                            if (polish_done(t, w2)) break;
-                        }
-                        const float d1 = ln_dist(zs), d2 = ln_dist(z2);
-                        if (d2 < d1) zs = z2;
-                        marg = fabsf(d2 - d1);
-                    }
-                    if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
-                    else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }
-                }
-                if (!pow_ok || !aby_ok || !abx_ok || !isfinite(zy.x + zy.y + zx.x + zx.y))
-                    fl |= kFlagNonconverged;
-                if (fminf(my, mx) < kTauSel) fl |= kFlagAmbiguous;
-
-                // ---- a6: Eq.(15) least-squares phase at the target pixel ----
-                // ẑ_x = e^{-jω_x}, ẑ_y = e^{jω_y}; basis e^{-j(ω_x o_k + ω_y o_i)} = ẑ_x^{o_k} conj(ẑ_y)^{o_i}
-                const float2 hx = cscale(zx, rsqrtf(cabs2(zx)));
-                const float2 hy = cscale(zy, rsqrtf(cabs2(zy)));
-                // row_i = Σ_k Γ(i,k)·tw_k = Σ_k re(g)·tw_k + im(g)·(j·tw_k)  (two FFMA2 per sample)
-                cx2 tw[M], twj[M];
-                {
-                    float2 p = make_float2(1.0f, 0.0f);
-#pragma unroll
-                    for (int k = 0; k < O0; ++k) p = cmul(p, cconj(hx));
-#pragma unroll
-                    for (int k = 0; k < M; ++k) {
-                        tw[k] = cx2_make(p.x, p.y);
-                        twj[k] = cx2_make(-p.y, p.x);
-                        p = cmul(p, hx);
-                    }
-                }
-                float2 q = make_float2(1.0f, 0.0f);
-#pragma unroll
-                for (int i = 0; i < O0; ++i) q = cmul(q, hy);
-                float2 csum = make_float2(0.0f, 0.0f);
-#pragma unroll 1
-                for (int i = 0; i < M; ++i) {
-                    cx2 row = 0ull;
-#pragma unroll
-                    for (int k = 0; k < M; ++k) {
-                        const float2 g = win[i * TW + k];
-                        row = fma2(cx2_bcast(g.x), tw[k], fma2(cx2_bcast(g.y), twj[k], row));
-                    }
-                    csum = cfma(cx2_f2(row), q, csum);
-                    q = cmul(q, cconj(hy));
-                }
-                if (!(cabs2(csum) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
-                float a = atan2f(csum.y, csum.x);
+                float2 zx, zy;
+                float a = roots_and_phase<M, TW, FB>(win, u, v, trace, pow_ok, fl, n_aby, n_abx, zx, zy);
                 // ---- a7: reference difference, wrap into (−π, π] ----
                 if (omx != nullptr) wx = -atan2f(zx.y, zx.x);       // Eq.(15): ω_x = −arg z_x
                 if (omy != nullptr) wy = atan2f(zy.y, zy.x);        //          ω_y =  arg z_y

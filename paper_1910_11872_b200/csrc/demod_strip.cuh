@@ -1,0 +1,324 @@
+// demod_strip.cuh — the paper-path thread-per-pixel kernel with a sliding covariance
+// ("strip kernel", window sizes M ≤ BOS_STRIP_MAX_M).
+//
+// Same per-pixel chain as demod_kernel.cuh (Algorithm 1: a2 R_y = Γ_wΓ_w^H,
+// a3 power iteration + v_1 = Γ_w^H u_1, a4 coefficients, a5 symmetric Aberth + selection,
+// a6 Eq.(15), a7 wrap(α − φ_ref)) and the same FP32 arithmetic, but a warp walks DOWN a
+// vertical strip of S image rows × 32 columns instead of across one row, so consecutive
+// pixels of a thread share M−1 of the M window rows:
+//
+//   R_y(py+1)(i, j) = R_y(py)(i+1, j+1)          for i, j ≤ M−2      (Eq.(4), rows ↔ y [R4])
+//
+// exactly — each entry is Σ_k Γ(row_a, k)·conj(Γ(row_b, k)) over the window's M columns, and
+// clamped border rows [R1] shift the same way.  Per pixel only the new last row R(M−1, ·) is
+// formed (M² complex MACs instead of M²(M+1)/2): the covariance drops from ≈17 % (M = 8) … 30 %
+// (M = 16) of the per-pixel flops to ≈3 %.  Each entry is summed over k in the same order as
+// the row kernel's full build, so R — and with it every output — is bitwise identical to
+// demod_kernel<M, false, false> (tests/test_gpu_strip.py).  A non-finite sample poisons exactly
+// the entries of its row and leaves with it: no rebuild is needed.
+//
+// Layout (one warp = 32 columns, lanes independent after staging):
+//  * halo tile per warp: (M+1) rows × (32+M−1) complex in shared memory — rows 0…M−1 the
+//    current window rows, row M the next row, prefetched with cp.async one step ahead; per
+//    step every lane shifts its own two columns up by one row (no cross-lane hazard);
+//  * R_y in registers while the pixel forms it and runs the power iteration (as in the row
+//    kernel); between pixels the (M−1)(M−2)/2 + M−1 entries that survive the shift wait in the
+//    thread's shared-memory slice (stride = threads per CTA: consecutive lanes → consecutive
+//    words), stored already shifted.  (A first version kept all of R_y in shared memory and ran
+//    the power iteration from there: 2·NOFF loads per iteration doubled the kernel's shared
+//    traffic and it measured 7 % slower than the row kernel at M = 8.);
+//  * work item = (frame, strip of S rows, 32-column block), one per 1-warp CTA: the hardware
+//    block scheduler refills an SM slot as soon as a warp finishes, so fast and slow strips
+//    balance (a persistent grid with equal row shares per warp reached 20.5 % of the 25 %
+//    theoretical occupancy at M = 8 — warps that finished early left their slots idle).
+#pragma once
+
+#include "demod_kernel.cuh"
+
+#ifndef BOS_STRIP_MAX_M
+#define BOS_STRIP_MAX_M 11
+#endif
+
+namespace bos {
+
+constexpr int kStripMaxM = BOS_STRIP_MAX_M;
+
+// warps per CTA (shared-memory granularity: the R slices grow as M²) and the register budget
+#ifndef BOS_STRIP_ROWS
+#define BOS_STRIP_ROWS 16        // S: rows per work item (fewer for small launches, see launch_strip)
+#endif
+#ifndef BOS_STRIP_MIN_ROWS
+#define BOS_STRIP_MIN_ROWS 8     // smaller launches run on the row kernel (launch_strip)
+#endif
+#ifndef BOS_STRIP_WARPS
+#define BOS_STRIP_WARPS 1
+#endif
+template <int M>
+constexpr int strip_warps() { return BOS_STRIP_WARPS; }
+// resident warps per SM the register budget is sized for (4 per SM partition → 128 registers,
+// 3 → 168, 2 → 255)
+template <int M>
+constexpr int strip_warps_per_sm() { return M <= 8 ? 16 : (M <= 11 ? 12 : 8); }
+template <int M>
+constexpr int strip_min_blocks() { return strip_warps_per_sm<M>() / strip_warps<M>(); }
+template <int M>
+constexpr size_t strip_smem_bytes() {
+    constexpr int NT = strip_warps<M>() * 32;
+    return (size_t)strip_warps<M>() * (M + 1) * (32 + M - 1) * sizeof(float2) +
+           (size_t)NT * ((M - 1) * (M - 2) / 2) * sizeof(cx2) + (size_t)NT * (M - 1) * sizeof(float);
+}
+
+// Row I of R_y over the window's M columns — entries (I, j), j < I, and the diagonal entry I —
+// summed over k in the row kernel's order (so every entry is bitwise the row kernel's).
+template <int M, int TW, int I>
+__device__ __forceinline__ void strip_new_row(const float2* win, float (&Rd)[M], cx2 (&Ro)[M * (M - 1) / 2]) {
+    constexpr int B = I * (I - 1) / 2;                 // tri_off(I, 0)
+    float d = 0.0f;
+#pragma unroll
+    for (int j = 0; j < I; ++j) Ro[B + j] = 0ull;
+#pragma unroll 1
+    for (int k = 0; k < M; ++k) {
+        const float2 gi = win[I * TW + k];
+        d = fmaf(gi.x, gi.x, fmaf(gi.y, gi.y, d));
+        const cx2 ci = cx2_make(gi.x, gi.y);
+        const cx2 cnj = mul2(cx2_make(gi.y, gi.x), cx2_make(1.0f, -1.0f));   // −j·a
+#pragma unroll
+        for (int j = 0; j < I; ++j) {
+            const float2 gj = win[j * TW + k];
+            Ro[B + j] = fma2(cx2_bcast(gj.x), ci, fma2(cx2_bcast(gj.y), cnj, Ro[B + j]));
+        }
+    }
+    Rd[I] = d;
+}
+
+// The carry between consecutive pixels of a thread, in its shared-memory slice (stride NT):
+// slot (i, j) of the next pixel = entry (i+1, j+1) of this one, i.e. only the (M−1)(M−2)/2
+// entries and M−1 diagonal values that survive the shift.
+template <int M, int NT>
+__device__ __forceinline__ void strip_store_carry(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2], cx2* Cs,
+                                                  float* Cds) {
+#pragma unroll
+    for (int i = 0; i + 1 < M; ++i) Cds[i * NT] = Rd[i + 1];
+#pragma unroll
+    for (int i = 1; i + 1 < M; ++i) {
+#pragma unroll
+        for (int j = 0; j < i; ++j) Cs[tri_off<M>(i, j) * NT] = Ro[tri_off<M>(i + 1, j + 1)];
+    }
+}
+
+template <int M, int NT>
+__device__ __forceinline__ void strip_load_carry(float (&Rd)[M], cx2 (&Ro)[M * (M - 1) / 2], const cx2* Cs,
+                                                 const float* Cds) {
+#pragma unroll
+    for (int i = 0; i + 1 < M; ++i) Rd[i] = Cds[i * NT];
+#pragma unroll
+    for (int i = 1; i + 1 < M; ++i) {
+#pragma unroll
+        for (int j = 0; j < i; ++j) Ro[tri_off<M>(i, j)] = Cs[tri_off<M>(i, j) * NT];
+    }
+}
+
+// The row kernel's power iteration (demod_kernel.cuh, a3) on R_y in registers: start
+// u_i = e^{jω̂ i}/√M from the lag-1 correlation, y = R u, stop at ‖Δu‖² < kPowerTol.
+// lam2 = ‖R u‖² of the converged step (λ1²), +inf when the cap was hit.
+template <int M>
+__device__ __forceinline__ int strip_power_iteration(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2],
+                                                     cx2 (&u)[M], bool& ok, float& lam2) {
+    float2 r1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
+    float2 e = make_float2(1.0f, 0.0f);
+    if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+    {
+        float2 t = make_float2(rsqrtf(float(M)), 0.0f);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            u[i] = cx2_make(t.x, t.y);
+            t = cmul(t, e);
+        }
+    }
+    lam2 = CUDART_INF_F;
+    ok = false;
+    int n = 0;
+    for (; n < kPowerMaxIt;) {
+        cx2 uj[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
+        cx2 y[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                const cx2 r = Ro[tri_off<M>(i, j)];
+                acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
+            }
+#pragma unroll
+            for (int j = i + 1; j < M; ++j) {
+                const cx2 r = Ro[tri_off<M>(j, i)];
+                acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
+            }
+            y[i] = acc;
+        }
+        float nrm2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+        float diff = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const cx2 yn = mul2(y[i], inv);
+            diff += cabs2(cx2_f2(sub2(yn, u[i])));
+            u[i] = yn;
+        }
+        ++n;
+        if (diff < kPowerTol) { ok = true; lam2 = nrm2; break; }
+    }
+    return n;
+}
+
+template <int M, bool COUNT>
+__global__ void __launch_bounds__(strip_warps<M>() * 32, strip_min_blocks<M>())
+demod_strip_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int S,
+                   const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
+                   float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
+    constexpr int WARPS = strip_warps<M>();
+    constexpr int NT = WARPS * 32;
+    constexpr int O0 = (M - 1) / 2;                 // o_i = i − O0  [R2]
+    constexpr int TW = kBX + M - 1;
+    constexpr int NOFF = M * (M - 1) / 2;
+    extern __shared__ __align__(16) unsigned char strip_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float2* tile = reinterpret_cast<float2*>(strip_smem) + warp * (M + 1) * TW;
+    constexpr int NCARRY = (M - 1) * (M - 2) / 2;
+    cx2* Cs = reinterpret_cast<cx2*>(reinterpret_cast<float2*>(strip_smem) + WARPS * (M + 1) * TW) + threadIdx.x;
+    float* Cds = reinterpret_cast<float*>(reinterpret_cast<cx2*>(reinterpret_cast<float2*>(strip_smem) +
+                                                                  WARPS * (M + 1) * TW) + NCARRY * NT) + threadIdx.x;
+    const size_t plane = (size_t)H * (size_t)W;
+    const int nbx = (W + kBX - 1) / kBX;
+    const int nstrip = (H + S - 1) / S;
+    const long long items = (long long)n_frames * nstrip * nbx;     // (frame, strip of S rows, 32-column block)
+    const long long wstride = (long long)gridDim.x * WARPS;
+
+    for (long long item = (long long)blockIdx.x * WARPS + warp; item < items; item += wstride) {
+        const int bx = (int)(item % nbx);
+        const long long rest = item / nbx;
+        const int f = (int)(rest / nstrip);
+        const int py0 = (int)(rest % nstrip) * S;
+        const int rows = min(S, H - py0);
+        const int x0 = bx * kBX, px = x0 + lane;
+        const float2* __restrict__ frame = frames + (size_t)f * plane;
+        const int gx0 = min(max(x0 - O0 + lane, 0), W - 1);
+        const int gx1 = min(max(x0 - O0 + lane + kBX, 0), W - 1);
+        // strip row r (0 … rows+M−2) ↔ image row clamp(py0 − O0 + r)  (a1, [R1])
+        auto load_row = [&](int r, float2* dst) {
+            const float2* __restrict__ row = frame + (size_t)min(max(py0 - O0 + r, 0), H - 1) * W;
+            cp_async8(dst + lane, row + gx0);
+            if (lane + kBX < TW) cp_async8(dst + lane + kBX, row + gx1);
+        };
+        __syncwarp();                                  // the previous item's reads of the tile are done
+#pragma unroll 1
+        for (int r = 0; r < M; ++r) load_row(r, tile + r * TW);
+        cp_async_commit();
+        for (int s = 0; s < rows; ++s) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (s > 0) {                               // window moves down one row: rows 1…M → 0…M−1
+#pragma unroll
+                for (int r = 0; r < M; ++r) {
+                    tile[r * TW + lane] = tile[(r + 1) * TW + lane];
+                    if (lane + kBX < TW) tile[r * TW + lane + kBX] = tile[(r + 1) * TW + lane + kBX];
+                }
+                __syncwarp();
+            }
+            if (s + 1 < rows) load_row(s + M, tile + M * TW);     // next step's new row (row M)
+            cp_async_commit();
+
+            const int py = py0 + s;
+            if (px < W) {
+                const float2* win = tile + lane;       // Γ_w(i,k) = win[i*TW + k]
+                uint8_t fl = 0;
+                if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
+                    fl |= kFlagBorder;
+                // ---- a2: R_y in registers: in full at the strip start, else the carry (the
+                // previous pixel's entries shifted by one row) + the new last row ----
+                float Rd[M];
+                cx2 Ro[NOFF > 0 ? NOFF : 1];
+                if (s == 0) {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) Rd[i] = 0.0f;
+#pragma unroll
+                    for (int t = 0; t < NOFF; ++t) Ro[t] = 0ull;
+                    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+#pragma unroll 1
+                    for (int k = 0; k < M; ++k) {   // the row kernel's full build (same order)
+                        cx2 col[M], colnj[M];
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            const float2 g = win[i * TW + k];
+                            col[i] = cx2_make(g.x, g.y);
+                            colnj[i] = mul2(cx2_make(g.y, g.x), kPosNeg);
+                            Rd[i] = fmaf(g.x, g.x, fmaf(g.y, g.y, Rd[i]));
+                        }
+#pragma unroll
+                        for (int i = 1; i < M; ++i) {
+#pragma unroll
+                            for (int j = 0; j < i; ++j) {
+                                cx2& r = Ro[tri_off<M>(i, j)];
+                                r = fma2(cx2_bcast(cx2_re(col[j])), col[i], fma2(cx2_bcast(cx2_im(col[j])), colnj[i], r));
+                            }
+                        }
+                    }
+                } else {
+                    strip_load_carry<M, NT>(Rd, Ro, Cs, Cds);
+                    strip_new_row<M, TW, M - 1>(win, Rd, Ro);
+                }
+                if (s + 1 < rows) strip_store_carry<M, NT>(Rd, Ro, Cs, Cds);
+                float trace = 0.0f;
+#pragma unroll
+                for (int i = 0; i < M; ++i) trace += Rd[i];
+
+                float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
+                int n_pow = 0, n_aby = 0, n_abx = 0;
+                if (!isfinite(trace)) {
+                    fl |= kFlagNonfinite;
+                    result = CUDART_NAN_F;
+                } else {
+                    // ---- a3: u_1 by power iteration (the row kernel's), v_1 = Γ_w^H u_1 / ‖·‖ ----
+                    cx2 u[M];
+                    bool pow_ok = false;
+                    float lam2;
+                    n_pow = strip_power_iteration<M>(Rd, Ro, u, pow_ok, lam2);
+                    if constexpr (!newton_stop<false, M>())
+                        if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
+                    float2 v[M];
+                    v1_from_window<M, TW>(win, u, v);
+                    // ---- a4 + a5 + a6 ----
+                    float2 zx, zy;
+                    float a = roots_and_phase<M, TW, false>(win, u, v, trace, pow_ok, fl, n_aby, n_abx, zx, zy);
+                    // ---- a7: reference difference, wrap into (−π, π] ----
+                    if (omx != nullptr) wx = -atan2f(zx.y, zx.x);       // Eq.(15): ω_x = −arg z_x
+                    if (omy != nullptr) wy = atan2f(zy.y, zy.x);        //          ω_y =  arg z_y
+                    if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
+                    if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
+                    if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
+                    result = a;
+                }
+                const size_t o = (size_t)f * plane + (size_t)py * W + px;
+                out[o] = result;
+                if (flags != nullptr) flags[o] = fl & uint8_t(~kFlagWeakInternal);
+                if (omx != nullptr) omx[o] = wx;
+                if (omy != nullptr) omy[o] = wy;
+                if (COUNT) {
+                    atomicAdd(counters + 0, 1ull);
+                    atomicAdd(counters + 1, (unsigned long long)n_pow);
+                    atomicAdd(counters + 2, (unsigned long long)n_aby);
+                    atomicAdd(counters + 3, (unsigned long long)n_abx);
+                }
+            }
+        }
+        cp_async_wait_all();
+    }
+}
+
+}  // namespace bos

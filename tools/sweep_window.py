@@ -83,7 +83,7 @@ def main():
             cnt = bosrm.bos_rootmusic_iteration_counts(frames[1:2], M)
             npx = cnt["pixels"]
             kpi, ky, kx = cnt["power_its"] / npx, cnt["aberth_y"] / npx, cnt["aberth_x"] / npx
-            fpx = bench.flops_per_pixel(M, kpi, ky, kx)
+            fpx = bench.flops_per_pixel(M, kpi, ky, kx, strip_rows=bench.strip_rows_for(M, T, w.H, w.W))
         tf = fpx * mpx * 1e6 / 1e12
         rng = np.random.default_rng(M)
         pix = (rng.integers(0, w.H, args.parity_px), rng.integers(0, w.W, args.parity_px))
