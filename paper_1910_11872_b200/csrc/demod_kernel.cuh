@@ -123,6 +123,14 @@ constexpr float kWeakNewtonRatio = BOS_WEAK_NEWTON_RATIO;
 #define BOS_WEAK_MODE 0     // 1: weak pixels start from kAberthLowSnrTol2; 0: per-pixel Newton-ratio stop
 #endif
 constexpr float kAberthLowSnrTol2 = 1e-4f;
+// From this window size the thread / strip kernels also apply the warp kernel's weak-tone rule
+// (λ1 < kLowSnrRatio·tr R_y → start from kAberthLowSnrTol2) on top of the Newton-ratio stop:
+// tools/stress_parity.py (M = 12…22, seed 7) found a 20 dB pixel at M = 20 on a small clamped
+// frame 0.037 rad off, and tests/test_gpu_strip.py a 0 dB pixel at M = 22 2.4 rad off.
+#ifndef BOS_WEAK_TIGHT_MIN_M
+#define BOS_WEAK_TIGHT_MIN_M 16
+#endif
+constexpr int kWeakTightMinM = BOS_WEAK_TIGHT_MIN_M;
 constexpr int kPolishMin = 2;         // Newton steps on the selected root after the sweeps:
 constexpr int kPolishMax = 6;         // at least 2, then until |Δz|² < kPolishTol2, at most 6
 constexpr float kPolishTol2 = 1e-12f;
@@ -599,11 +607,17 @@ __device__ __forceinline__ void cov_pass_smem(const float2* win, cx2* Rs) {
 }
 
 // Power iteration as power_iteration() with R's strict lower triangle read from Rs.
-template <int M>
-__device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const cx2* Rs, cx2 (&u)[M], bool& ok) {
+// An empty asm with a memory clobber: the compiler may not move shared-memory accesses across
+// it.  Unrolled sweeps over a triangle held in shared memory otherwise get all their loads
+// hoisted to the top (independent addresses) and hold the whole triangle in registers.
+__device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
+
+template <int M, int STRIDE = kThreads, bool FENCE = false>
+__device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const cx2* Rs, cx2 (&u)[M], bool& ok,
+                                                    float* lam2_out = nullptr) {
     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Rs[tri_off<M>(i + 1, i) * kThreads]));
+    for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Rs[tri_off<M>(i + 1, i) * STRIDE]));
     float2 e = make_float2(1.0f, 0.0f);
     if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
     {
@@ -626,9 +640,10 @@ __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const 
         // each stored R_ij (i > j) serves y_i += R_ij u_j and y_j += conj(R_ij) u_i
 #pragma unroll
         for (int i = 1; i < M; ++i) {
+            if constexpr (FENCE) compiler_fence();   // one row's loads in flight, not the whole triangle
 #pragma unroll
             for (int j = 0; j < i; ++j) {
-                const cx2 r = Rs[tri_off<M>(i, j) * kThreads];
+                const cx2 r = Rs[tri_off<M>(i, j) * STRIDE];
                 y[i] = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], y[i]));
                 y[j] = fma2(cx2_bcast(cx2_re(r)), u[i], fma2(cx2_bcast(-cx2_im(r)), uj[i], y[j]));
             }
@@ -645,7 +660,11 @@ __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const 
             u[i] = yn;
         }
         ++n;
-        if (diff < kPowerTol) { ok = true; break; }
+        if (diff < kPowerTol) {
+            ok = true;
+            if (lam2_out != nullptr) *lam2_out = nrm2;     // ‖R u‖² = λ1² at convergence
+            break;
+        }
     }
     return n;
 }
@@ -681,7 +700,7 @@ __device__ __forceinline__ void v1_from_window(const float2* win, const cx2 (&u)
 // selection + polish (+ safety nets) → Eq.(15) least-squares phase.  Sets NONCONVERGED,
 // AMBIGUOUS and LOW_AMPLITUDE in fl; returns the raw α (before the reference difference) and
 // the selected roots zx (x axis, from v_1) and zy (y axis, from u_1).
-template <int M, int TW, bool FB>
+template <int M, int TW, bool FB, bool WEAK_TIGHT = false>
 __device__ __forceinline__ float roots_and_phase(const float2* win, const cx2 (&u)[M], const float2 (&v)[M], float trace,
                                                  bool pow_ok, uint8_t& fl, int& n_aby, int& n_abx, float2& zx_out,
                                                  float2& zy_out) {
@@ -709,7 +728,7 @@ __device__ __forceinline__ float roots_and_phase(const float2* win, const cx2 (&
         int its = 0;
         float marg = CUDART_INF_F;
         float2 zs, z2;
-        float tol2 = (BOS_WEAK_MODE == 1 && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
+        float tol2 = ((BOS_WEAK_MODE == 1 || WEAK_TIGHT) && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
 #pragma unroll 1
         for (int attempt = 0;; ++attempt) {
             its += aberth_sym<N, newton_stop<FB, M>()>(c, z, ok, tol2, BOS_WEAK_MODE == 0 && (fl & kFlagWeakInternal));
@@ -750,6 +769,130 @@ __device__ __forceinline__ float roots_and_phase(const float2* win, const cx2 (&
             const float d1 = ln_dist(zs), d2 = ln_dist(z2);
             if (d2 < d1) zs = z2;
             marg = fabsf(d2 - d1);
+        }
+        if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
+        else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }
+    }
+    if (!pow_ok || !aby_ok || !abx_ok || !isfinite(zy.x + zy.y + zx.x + zx.y))
+        fl |= kFlagNonconverged;
+    if (fminf(my, mx) < kTauSel) fl |= kFlagAmbiguous;
+
+    // ---- a6: Eq.(15) least-squares phase at the target pixel ----
+    // ẑ_x = e^{-jω_x}, ẑ_y = e^{jω_y}; basis e^{-j(ω_x o_k + ω_y o_i)} = ẑ_x^{o_k} conj(ẑ_y)^{o_i}
+    const float2 hx = cscale(zx, rsqrtf(cabs2(zx)));
+    const float2 hy = cscale(zy, rsqrtf(cabs2(zy)));
+    // row_i = Σ_k Γ(i,k)·tw_k = Σ_k re(g)·tw_k + im(g)·(j·tw_k)  (two FFMA2 per sample)
+    cx2 tw[M], twj[M];
+    {
+        float2 p = make_float2(1.0f, 0.0f);
+#pragma unroll
+        for (int k = 0; k < O0; ++k) p = cmul(p, cconj(hx));
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            tw[k] = cx2_make(p.x, p.y);
+            twj[k] = cx2_make(-p.y, p.x);
+            p = cmul(p, hx);
+        }
+    }
+    float2 q = make_float2(1.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i < O0; ++i) q = cmul(q, hy);
+    float2 csum = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+    for (int i = 0; i < M; ++i) {
+        cx2 row = 0ull;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            const float2 g = win[i * TW + k];
+            row = fma2(cx2_bcast(g.x), tw[k], fma2(cx2_bcast(g.y), twj[k], row));
+        }
+        csum = cfma(cx2_f2(row), q, csum);
+        q = cmul(q, cconj(hy));
+    }
+    if (!(cabs2(csum) >= kLowAmp * kLowAmp * float(M * M) * trace)) fl |= kFlagLowAmplitude;
+    float a = atan2f(csum.y, csum.x);
+    zx_out = zx;
+    zy_out = zy;
+    return a;
+}
+
+// roots_and_phase for the paper path with v_1 = Γ_w^H u_1/‖·‖ formed inside the axis loop when
+// the x axis starts (the strip kernels): only u stays live across the rooting of both axes —
+// with v_1 and a copy of u both live (roots_and_phase) the rolled axis loop carried 4M extra
+// registers through both Aberth runs.  Same arithmetic, bitwise the same result.
+template <int M, int TW, bool FB, bool WEAK_TIGHT = false>
+__device__ __forceinline__ float roots_and_phase_jit(const float2* win, const cx2 (&u)[M], float trace,
+                                                 bool pow_ok, uint8_t& fl, int& n_aby, int& n_abx, float2& zx_out,
+                                                 float2& zy_out) {
+    constexpr int N = 2 * M - 2;
+    constexpr int O0 = (M - 1) / 2;
+
+    // ---- a4 + a5, y axis (u_1) then x axis (v_1), one rolled loop ----
+    float2 zy = make_float2(0.0f, 0.0f), zx = make_float2(0.0f, 0.0f);
+    float my = CUDART_INF_F, mx = CUDART_INF_F;
+    bool aby_ok = false, abx_ok = false;
+#pragma unroll 1
+    for (int axis = 0; axis < 2; ++axis) {
+        float2 q[M];
+        if (axis == 0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) q[i] = cx2_f2(u[i]);
+        } else {
+            v1_from_window<M, TW>(win, u, q);      // v_1, formed when the x axis needs it
+        }
+        cx2 c[N + 1];
+        const float2 rot = music_coeffs<M>(q, c);
+        cx2 z[N / 2];       // the inside half of the rotated template
+#pragma unroll
+        for (int j = 0; j < N / 2; ++j) z[j] = f2_cx2(cmul(kTemplateRoots[bos_template_offset(M) + j], rot));
+        bool ok = false;
+        int its = 0;
+        float marg = CUDART_INF_F;
+        float2 zs, z2, zsel;
+        // WEAK_TIGHT (large windows): a weak-tone window starts from the tight tolerance, the
+        // warp kernel's rule (kLowSnrRatio) — with the Newton-ratio stop alone the loose sweeps
+        // misplaced a 0 dB pixel at M = 22 (2.4 rad, tests/test_gpu_strip.py)
+        float tol2 = ((BOS_WEAK_MODE == 1 || WEAK_TIGHT) && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
+        // roots_and_phase's attempt loop and runner-up polish as one loop with ONE copy of the
+        // polish code (the thread kernels are instruction-cache bound at M ≥ 13: ncu no_inst
+        // stalls 23 %):  stage 0: loose sweeps, polish the selected root;  1: tight sweeps
+        // after a failed check, polish again;  2: polish the runner-up of a near tie.
+        int stage = 0;
+#pragma unroll 1
+        for (;;) {
+            if (stage < 2) {
+                its += aberth_sym<N, newton_stop<FB, M>()>(c, z, ok, tol2, BOS_WEAK_MODE == 0 && (fl & kFlagWeakInternal));
+                zs = select_root<N / 2>(z, marg, z2);
+                zsel = zs;
+            }
+            float2 zt = stage < 2 ? zs : z2;
+#pragma unroll 1
+            for (int t = 0; t < kPolishMax; ++t) {
+                const float2 w = polish_step<N>(c, zt);
+                const float w2 = cabs2(w);
+                if (w2 < 1e30f) zt = csub(zt, w);
+                if (polish_done(t, w2)) break;
+            }
+            if (stage < 2) {
+                zs = zt;
+                const float dsel = ln_dist(zs), dsec = ln_dist(z2) - 1e-3f;
+                if (stage == 0 && (!(dsel <= dsec || marg == CUDART_INF_F) ||
+                                   !(cabs2(csub(zs, zsel)) <= kMoved2))) {
+                    tol2 = kAberthTightTol2;
+                    stage = 1;
+                    continue;
+                }
+                if (marg < kRefineMargin) {
+                    stage = 2;
+                    continue;
+                }
+                break;
+            }
+            z2 = zt;
+            const float d1 = ln_dist(zs), d2 = ln_dist(z2);
+            if (d2 < d1) zs = z2;
+            marg = fabsf(d2 - d1);
+            break;
         }
         if (axis == 0) { zy = zs; my = marg; aby_ok = ok; n_aby = its; }
         else { zx = zs; mx = marg; abx_ok = ok; n_abx = its; }
@@ -949,8 +1092,11 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 cx2 u[M];
                 bool pow_ok = false;
                 float2 v[M];
+                float lam2s = CUDART_INF_F;            // λ1² of the kRs power iteration
                 if constexpr (kRs) {
-                    n_pow = power_iteration_smem<M>(Rd, Rs, u, pow_ok);
+                    n_pow = power_iteration_smem<M, kThreads, true>(Rd, Rs, u, pow_ok, &lam2s);
+                    if constexpr (!FB && M >= kWeakTightMinM)
+                        if (lam2s < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
                 }
                 if constexpr (!FB) {
                     // ---- a3: dominant eigenvector of R_y by power iteration ----
@@ -1005,8 +1151,11 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         ++n_pow;
                         if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
                     }
-                    if constexpr (!newton_stop<FB, M>())   // weak-tone window (see newton_stop); a flag bit, not a register
+                    if constexpr (!newton_stop<FB, M>()) {  // weak-tone window (see newton_stop); a flag bit, not a register
                         if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
+                    } else if constexpr (M >= kWeakTightMinM) {   // see kWeakTightMinM
+                        if (lam2 < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
+                    }
                     }
                     v1_from_window<M, TW>(win, u, v);
                 } else {
@@ -1024,7 +1173,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                     for (int k = 0; k < M; ++k) v[k] = cconj(cx2_f2(sv[k]));
                 }
                 float2 zx, zy;
-                float a = roots_and_phase<M, TW, FB>(win, u, v, trace, pow_ok, fl, n_aby, n_abx, zx, zy);
+                float a = roots_and_phase<M, TW, FB, (!FB && M >= kWeakTightMinM)>(win, u, v, trace, pow_ok, fl, n_aby,
+                                                                                   n_abx, zx, zy);
                 // ---- a7: reference difference, wrap into (−π, π] ----
                 if (omx != nullptr) wx = -atan2f(zx.y, zx.x);       // Eq.(15): ω_x = −arg z_x
                 if (omy != nullptr) wy = atan2f(zy.y, zy.x);        //          ω_y =  arg z_y

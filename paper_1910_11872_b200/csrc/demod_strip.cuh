@@ -36,7 +36,7 @@
 #include "demod_kernel.cuh"
 
 #ifndef BOS_STRIP_MAX_M
-#define BOS_STRIP_MAX_M 11
+#define BOS_STRIP_MAX_M 14
 #endif
 
 namespace bos {
@@ -58,7 +58,7 @@ constexpr int strip_warps() { return BOS_STRIP_WARPS; }
 // resident warps per SM the register budget is sized for (4 per SM partition → 128 registers,
 // 3 → 168, 2 → 255)
 template <int M>
-constexpr int strip_warps_per_sm() { return M <= 8 ? 16 : (M <= 11 ? 12 : 8); }
+constexpr int strip_warps_per_sm() { return M <= 8 ? 16 : (M <= 11 ? 12 : 8); }   // 8: 255 registers
 template <int M>
 constexpr int strip_min_blocks() { return strip_warps_per_sm<M>() / strip_warps<M>(); }
 template <int M>
@@ -289,16 +289,251 @@ demod_strip_kernel(const float2* __restrict__ frames, int n_frames, int H, int W
                     bool pow_ok = false;
                     float lam2;
                     n_pow = strip_power_iteration<M>(Rd, Ro, u, pow_ok, lam2);
-                    if constexpr (!newton_stop<false, M>())
+                    if constexpr (!newton_stop<false, M>()) {
                         if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
-                    float2 v[M];
-                    v1_from_window<M, TW>(win, u, v);
-                    // ---- a4 + a5 + a6 ----
+                    } else if constexpr (M >= kWeakTightMinM) {
+                        if (lam2 < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
+                    }
+                    // ---- v_1 = Γ_w^H u_1/‖·‖, a4 + a5 + a6 ----
                     float2 zx, zy;
-                    float a = roots_and_phase<M, TW, false>(win, u, v, trace, pow_ok, fl, n_aby, n_abx, zx, zy);
+                    float a = roots_and_phase_jit<M, TW, false, (M >= kWeakTightMinM)>(win, u, trace, pow_ok, fl, n_aby,
+                                                                                       n_abx, zx, zy);
                     // ---- a7: reference difference, wrap into (−π, π] ----
                     if (omx != nullptr) wx = -atan2f(zx.y, zx.x);       // Eq.(15): ω_x = −arg z_x
                     if (omy != nullptr) wy = atan2f(zy.y, zy.x);        //          ω_y =  arg z_y
+                    if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
+                    if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
+                    if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
+                    result = a;
+                }
+                const size_t o = (size_t)f * plane + (size_t)py * W + px;
+                out[o] = result;
+                if (flags != nullptr) flags[o] = fl & uint8_t(~kFlagWeakInternal);
+                if (omx != nullptr) omx[o] = wx;
+                if (omy != nullptr) omy[o] = wy;
+                if (COUNT) {
+                    atomicAdd(counters + 0, 1ull);
+                    atomicAdd(counters + 1, (unsigned long long)n_pow);
+                    atomicAdd(counters + 2, (unsigned long long)n_aby);
+                    atomicAdd(counters + 3, (unsigned long long)n_abx);
+                }
+            }
+        }
+        cp_async_wait_all();
+    }
+}
+
+
+// ---- Larger windows (BOS_STRIP_RS_MIN_M ≤ M ≤ BOS_STRIP_RS_MAX_M): R_y never fits the registers
+// beside the rooting state, so it lives in the thread's shared-memory slice for good (as the row
+// kernel's kRsmem path): full at the strip start, then shifted in place (ascending entry order:
+// every source is read before any later write reaches it) plus the new last row, and the power
+// iteration reads it from there.  Order of the power-iteration sums: the row kernel's for the
+// same M (registers below BOS_RSMEM_MIN_M, power_iteration_smem from it), so the outputs stay
+// bitwise the row kernel's.
+#ifndef BOS_STRIP_RS_MIN_M
+#define BOS_STRIP_RS_MIN_M 16
+#endif
+#ifndef BOS_STRIP_RS_MAX_M
+#define BOS_STRIP_RS_MAX_M 22
+#endif
+constexpr int kStripWeakTightMinM = kWeakTightMinM;     // demod_kernel.cuh
+constexpr int kStripRsMinM = BOS_STRIP_RS_MIN_M;
+constexpr int kStripRsMaxM = BOS_STRIP_RS_MAX_M;
+
+template <int M>
+constexpr size_t strip_rs_smem_bytes() {      // one warp per CTA
+    return (size_t)(M + 1) * (32 + M - 1) * sizeof(float2) + (size_t)32 * (M * (M - 1) / 2) * sizeof(cx2) +
+           (size_t)32 * M * sizeof(float);
+}
+template <int M>
+constexpr int strip_rs_min_blocks() {         // what the shared memory admits (≈ 227 KB per SM), ≤ 8 (255 registers)
+    constexpr int b = (int)(227 * 1024 / (strip_rs_smem_bytes<M>() + 1024));
+    return b < 1 ? 1 : (b > 8 ? 8 : b);
+}
+
+// row I of R_y (entries (I, j), j < I, and the diagonal I) over the window, to the slice
+template <int M, int TW, int I>
+__device__ __forceinline__ void strip_rs_row(const float2* win, cx2* Rs, float* Rds) {
+    constexpr int B = I * (I - 1) / 2;
+    cx2 acc[I > 0 ? I : 1];
+    float d = 0.0f;
+#pragma unroll
+    for (int j = 0; j < I; ++j) acc[j] = 0ull;
+#pragma unroll 1
+    for (int k = 0; k < M; ++k) {
+        const float2 gi = win[I * TW + k];
+        d = fmaf(gi.x, gi.x, fmaf(gi.y, gi.y, d));
+        const cx2 ci = cx2_make(gi.x, gi.y);
+        const cx2 cnj = mul2(cx2_make(gi.y, gi.x), cx2_make(1.0f, -1.0f));
+#pragma unroll
+        for (int j = 0; j < I; ++j) {
+            const float2 gj = win[j * TW + k];
+            acc[j] = fma2(cx2_bcast(gj.x), ci, fma2(cx2_bcast(gj.y), cnj, acc[j]));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < I; ++j) Rs[(B + j) * 32] = acc[j];
+    Rds[I * 32] = d;
+}
+template <int M, int TW, int I = 0>
+__device__ __forceinline__ void strip_rs_all(const float2* win, cx2* Rs, float* Rds) {
+    if constexpr (I < M) {
+        strip_rs_row<M, TW, I>(win, Rs, Rds);
+        strip_rs_all<M, TW, I + 1>(win, Rs, Rds);
+    }
+}
+
+template <int M, bool COUNT>
+__global__ void __launch_bounds__(32, strip_rs_min_blocks<M>())
+demod_strip_rs_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int S,
+                      const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
+                      float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
+    constexpr int O0 = (M - 1) / 2;
+    constexpr int TW = kBX + M - 1;
+    constexpr int NOFF = M * (M - 1) / 2;
+    extern __shared__ __align__(16) unsigned char strip_smem[];
+    const int lane = threadIdx.x;
+    float2* tile = reinterpret_cast<float2*>(strip_smem);
+    cx2* Rs = reinterpret_cast<cx2*>(tile + (M + 1) * TW) + lane;           // entry t at Rs[t·32]
+    float* Rds = reinterpret_cast<float*>(reinterpret_cast<cx2*>(tile + (M + 1) * TW) + NOFF * 32) + lane;
+    const size_t plane = (size_t)H * (size_t)W;
+    const int nbx = (W + kBX - 1) / kBX;
+    const int nstrip = (H + S - 1) / S;
+    const long long items = (long long)n_frames * nstrip * nbx;
+
+    for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+        const int bx = (int)(item % nbx);
+        const long long rest = item / nbx;
+        const int f = (int)(rest / nstrip);
+        const int py0 = (int)(rest % nstrip) * S;
+        const int rows = min(S, H - py0);
+        const int x0 = bx * kBX, px = x0 + lane;
+        const float2* __restrict__ frame = frames + (size_t)f * plane;
+        const int gx0 = min(max(x0 - O0 + lane, 0), W - 1);
+        const int gx1 = min(max(x0 - O0 + lane + kBX, 0), W - 1);
+        auto load_row = [&](int r, float2* dst) {
+            const float2* __restrict__ row = frame + (size_t)min(max(py0 - O0 + r, 0), H - 1) * W;
+            cp_async8(dst + lane, row + gx0);
+            if (lane + kBX < TW) cp_async8(dst + lane + kBX, row + gx1);
+        };
+        __syncwarp();
+#pragma unroll 1
+        for (int r = 0; r < M; ++r) load_row(r, tile + r * TW);
+        cp_async_commit();
+        for (int s = 0; s < rows; ++s) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (s > 0) {
+#pragma unroll 1
+                for (int r = 0; r < M; ++r) {
+                    tile[r * TW + lane] = tile[(r + 1) * TW + lane];
+                    if (lane + kBX < TW) tile[r * TW + lane + kBX] = tile[(r + 1) * TW + lane + kBX];
+                }
+                __syncwarp();
+            }
+            if (s + 1 < rows) load_row(s + M, tile + M * TW);
+            cp_async_commit();
+
+            const int py = py0 + s;
+            if (px < W) {
+                const float2* win = tile + lane;
+                uint8_t fl = 0;
+                if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
+                    fl |= kFlagBorder;
+                // ---- a2: R_y in the slice: in full at the strip start, else shift + new last row ----
+                if (s == 0) {
+                    strip_rs_all<M, TW>(win, Rs, Rds);
+                } else {
+#pragma unroll
+                    for (int i = 0; i + 1 < M; ++i) Rds[i * 32] = Rds[(i + 1) * 32];
+#pragma unroll
+                    for (int i = 1; i + 1 < M; ++i) {
+                        compiler_fence();           // row by row (see compiler_fence)
+#pragma unroll
+                        for (int j = 0; j < i; ++j) Rs[tri_off<M>(i, j) * 32] = Rs[tri_off<M>(i + 1, j + 1) * 32];
+                    }
+                    strip_rs_row<M, TW, M - 1>(win, Rs, Rds);
+                }
+                float Rd[M];
+                float trace = 0.0f;
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    Rd[i] = Rds[i * 32];
+                    trace += Rd[i];
+                }
+                float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
+                int n_pow = 0, n_aby = 0, n_abx = 0;
+                if (!isfinite(trace)) {
+                    fl |= kFlagNonfinite;
+                    result = CUDART_NAN_F;
+                } else {
+                    cx2 u[M];
+                    bool pow_ok = false;
+                    float lam2 = CUDART_INF_F;          // ‖R u‖² at convergence (row-order branch)
+                    if constexpr (M >= BOS_RSMEM_MIN_M) {
+                        n_pow = power_iteration_smem<M, 32, true>(Rd, Rs, u, pow_ok, &lam2);
+                    } else {
+                        // the row kernel's register order, R read from the slice (entries twice)
+                        float2 r1 = make_float2(0.0f, 0.0f);
+#pragma unroll
+                        for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Rs[tri_off<M>(i + 1, i) * 32]));
+                        float2 e = make_float2(1.0f, 0.0f);
+                        if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
+                        {
+                            float2 t = make_float2(rsqrtf(float(M)), 0.0f);
+#pragma unroll
+                            for (int i = 0; i < M; ++i) {
+                                u[i] = cx2_make(t.x, t.y);
+                                t = cmul(t, e);
+                            }
+                        }
+                        for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                            cx2 uj[M];
+#pragma unroll
+                            for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
+                            cx2 y[M];
+#pragma unroll
+                            for (int i = 0; i < M; ++i) {
+                                compiler_fence();
+                                cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
+#pragma unroll
+                                for (int j = 0; j < i; ++j) {
+                                    const cx2 r = Rs[tri_off<M>(i, j) * 32];
+                                    acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
+                                }
+#pragma unroll
+                                for (int j = i + 1; j < M; ++j) {
+                                    const cx2 r = Rs[tri_off<M>(j, i) * 32];
+                                    acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
+                                }
+                                y[i] = acc;
+                            }
+                            float nrm2 = 0.0f;
+#pragma unroll
+                            for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+                            const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+                            float diff = 0.0f;
+#pragma unroll
+                            for (int i = 0; i < M; ++i) {
+                                const cx2 yn = mul2(y[i], inv);
+                                diff += cabs2(cx2_f2(sub2(yn, u[i])));
+                                u[i] = yn;
+                            }
+                            ++n_pow;
+                            if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
+                        }
+                    }
+                    if constexpr (!newton_stop<false, M>()) {   // weak-tone window (demod_kernel.cuh, newton_stop)
+                        if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
+                    } else if constexpr (M >= kStripWeakTightMinM) {   // the warp kernel's weak-tone rule
+                        if (lam2 < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
+                    }
+                    float2 zx, zy;
+                    float a = roots_and_phase_jit<M, TW, false, (M >= kStripWeakTightMinM)>(win, u, trace, pow_ok, fl,
+                                                                                            n_aby, n_abx, zx, zy);
+                    if (omx != nullptr) wx = -atan2f(zx.y, zx.x);
+                    if (omy != nullptr) wy = atan2f(zy.y, zy.x);
                     if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
                     if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
                     if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;

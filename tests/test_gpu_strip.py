@@ -1,5 +1,7 @@
-"""The strip kernel (csrc/demod_strip.cuh: a warp walks down a strip of rows and slides R_y by
-one row per pixel) against the row kernel (csrc/demod_kernel.cuh: R_y formed in full per
+"""The strip kernels (csrc/demod_strip.cuh: a warp walks down a strip of rows and slides R_y by
+one row per pixel; R_y in registers up to M = 14, in the thread's shared-memory slice for
+M = 16…22; M = 15 and M ≥ 23 stay on the row / warp kernels; the row kernel exists up to
+M = 20, so M = 21, 22 are checked against the FP64 oracle here instead) against the row kernel (csrc/demod_kernel.cuh: R_y formed in full per
 pixel): R_y(py+1)(i, j) = R_y(py)(i+1, j+1) exactly (Eq.(4), rows ↔ y), every entry is summed
 in the same order, so phase, flags and ω maps must be BITWISE identical — on ragged frames,
 at every strip height the launcher picks (small launches: S = 4; large: S = 32), with clamped
@@ -10,7 +12,10 @@ import numpy as np
 import pytest
 import torch
 
+from oracle import rootmusic as R
 from paper_1910_11872_b200 import bosrm, synth
+
+from .parity_util import assert_excluded_valid, assert_parity
 
 DEV = "cuda"
 
@@ -35,7 +40,7 @@ def _assert_same(a, b, what):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("M", [3, 4, 5, 6, 7, 8, 9, 10, 11])
+@pytest.mark.parametrize("M", [3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 16, 17, 18, 19, 20])
 def test_strip_kernel_bitwise_equals_row_kernel_small(M, monkeypatch):
     """Ragged 3-frame stack (H, W not multiples of the strip / 32-column block), 10 dB, 0 dB
     and a NaN sample: the small launch makes the launcher pick the shortest strips (S = 2)."""
@@ -50,7 +55,7 @@ def test_strip_kernel_bitwise_equals_row_kernel_small(M, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("M", [8, 9, 11])
+@pytest.mark.parametrize("M", [8, 9, 11, 12, 14, 16, 17, 20])
 def test_strip_kernel_bitwise_equals_row_kernel_large(M, monkeypatch):
     """A launch large enough for the full strip height (16 rows) on 1024² frames."""
     w = synth.workload("C3", seed=11, window_len=M)
@@ -72,3 +77,21 @@ def test_strip_kernel_is_the_default_on_large_launches(monkeypatch):
     monkeypatch.setenv("BOS_THREAD_KERNEL", "strip")
     strip = bosrm.bos_rootmusic_demod(fr, 8)[0]
     assert torch.equal(_bits(auto), _bits(strip))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M", [21, 22])
+def test_strip_rs_kernel_parity_beyond_the_row_kernel(M, monkeypatch):
+    """M = 21, 22 run on the shared-memory strip kernel (no row kernel there to compare
+    bitwise): element-by-element parity with the FP64 oracle on a ragged 10 dB and a 0 dB frame
+    (forced onto the strip kernel: the small launch gives 2-row strips, so both the full build
+    and the slide are exercised)."""
+    monkeypatch.setenv("BOS_THREAD_KERNEL", "strip")
+    w = synth.workload("C3", H=M + 37, W=M + 60, seed=13)
+    for t, snr in ((2, 10.0), (3, 0.0)):
+        f = synth.make_frame(w, t, snr_db=snr)
+        g, gfl, wx, wy = bosrm.bos_rootmusic_demod_ex(f.unsqueeze(0).to(DEV), M, flags=True, omega=True)
+        g, gfl, wx, wy = (x[0].cpu().numpy() for x in (g, gfl, wx, wy))
+        o, ofl = R.demod_frame(f.numpy(), M)
+        assert_parity(g, o, ofl, f"strip_rs M={M} {snr} dB", gpu_flags=gfl)
+        assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"strip_rs M={M} {snr} dB")

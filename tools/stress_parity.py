@@ -20,11 +20,12 @@ from oracle import rootmusic as R  # noqa: E402
 from paper_1910_11872_b200 import bosrm, synth  # noqa: E402
 
 
-def draw_cases(seed, n):
-    """The random case sequence of a seed: dicts with M, H, W, snr, workload, t, wseed."""
+def draw_cases(seed, n, min_m=3, max_m=32):
+    """The random case sequence of a seed: dicts with M, H, W, snr, workload, t, wseed (the
+    default M range 3…32 reproduces the sequences quoted in DESIGN.md)."""
     rng = np.random.default_rng(seed)
     for c in range(n):
-        M = int(rng.integers(3, 33))
+        M = int(rng.integers(min_m, max_m + 1))
         H = int(rng.integers(max(M, 8), 96))
         W = int(rng.integers(max(M, 8), 120))
         snr = float(rng.choice([-5.0, 0.0, 5.0, 10.0, 20.0, 40.0, np.inf]))
@@ -65,9 +66,11 @@ def main():
     ap.add_argument("--budget-s", type=float, default=600.0)
     ap.add_argument("--variant", default="paper", choices=["paper", "fb", "ss", "ss_fb"])
     ap.add_argument("--subarray", type=int, default=3, help="spatial-smoothing subarray m (ss variants)")
+    ap.add_argument("--min-m", type=int, default=3)
+    ap.add_argument("--max-m", type=int, default=32)
     args = ap.parse_args()
     bad, worst, t0, c = [], 0.0, time.time(), -1
-    for k in draw_cases(args.seed, args.cases):
+    for k in draw_cases(args.seed, args.cases, args.min_m, args.max_m):
         if time.time() - t0 > args.budget_s:
             break
         c = k["case"]
