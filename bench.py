@@ -74,47 +74,66 @@ def peaks():
         return {}
 
 
-STRIP_MAX_M = 11     # BOS_STRIP_MAX_M (csrc/demod_strip.cuh): paper-path windows on the strip kernel
 STRIP_ROWS = 16      # BOS_STRIP_ROWS: rows per strip work item on large launches (launch_strip)
 STRIP_MIN_ROWS = 8   # BOS_STRIP_MIN_ROWS: launches that would get shorter strips run the row kernel
 
 
+def strip_kind(M: int) -> int:
+    """csrc/demod_strip.cuh strip_kind<M>(): 1 = R_y slid in registers, 2 = no R_y (implicit
+    power iteration y = Γ_w(Γ_w^H u))."""
+    return 1 if (M <= 10 or M in (12, 13)) else 2
+
+
 def covariance_flops(M: int, strip_rows: int | None) -> float:
-    """R_y = Γ_wΓ_w^H per pixel: 4M³ when formed in full (row / warp kernels); on the strip kernel
-    one full build per S-row strip and, for the other S−1 rows, only the new last row
-    (M−1 complex MACs × M columns + the real diagonal entry: 8M(M−1) + 4M)."""
+    """R_y = Γ_wΓ_w^H per pixel: 4M³ when formed in full (row / warp kernels); on the register
+    strip kernel one full build per S-row strip and, for the other S−1 rows, only the new last
+    row (M−1 complex MACs × M columns + the real diagonal entry: 8M(M−1) + 4M)."""
     full = 4.0 * M ** 3
     if not strip_rows:
         return full
     return (full + (strip_rows - 1) * (8.0 * M * (M - 1) + 4.0 * M)) / strip_rows
 
 
-def flops_per_pixel(M: int, k_pi: float, k_aby: float, k_abx: float, strip_rows: int | None = None) -> float:
-    """Algorithmic FP32 flops per pixel of the path, FMA = 2 flops:
-    covariance (covariance_flops); power iteration k_pi·(8M²+12M); v_1 = Γ^H u_1 8M²+4M; two
-    autocorrelation polynomials 8M(M−1); symmetric Aberth sweeps k·(n/2)·(25n+21) with
-    n = 2M−2 (per tracked root: Horner for P and P′ 16n, n−1 reciprocal terms at 9 flops,
-    mirror + update 30); selection 2·20(n/2); 2 Newton polish steps per axis 2·2·(16n+30);
-    Eq.(15) 8M²+8M+20."""
+def flops_per_pixel(M: int, k_pi: float, k_aby: float, k_abx: float, strip_rows: int | None = None,
+                    kind: int | None = None) -> float:
+    """Algorithmic FP32 flops per pixel of the path, FMA = 2 flops.
+    R_y and the power iteration, by kernel: explicit R_y (row / warp kernels, register strip
+    kernel) — covariance (covariance_flops) + k_pi·(8M²+12M); implicit (kind 2, no R_y) — one
+    pass for tr R_y and Σ R[i+1][i] 12M², then k_pi·(16M²+12M) (Γ_w^H u and Γ_w t: 2M² complex
+    MACs).  Common: v_1 = Γ^H u_1 8M²+4M; two autocorrelation polynomials 8M(M−1); symmetric
+    Aberth sweeps k·(n/2)·(25n+21) with n = 2M−2 (per tracked root: Horner for P and P′ 16n,
+    n−1 reciprocal terms at 9 flops, mirror + update 30); selection 2·20(n/2); 2 Newton polish
+    steps per axis 2·2·(16n+30); Eq.(15) 8M²+8M+20."""
     n = 2 * M - 2
     polish = 2 * 2 * (16.0 * n + 30.0)       # 2 Newton steps on the selected root, 2 axes
-    return (covariance_flops(M, strip_rows) + k_pi * (8.0 * M * M + 12.0 * M) + 8.0 * M * M + 4.0 * M
+    if kind == 2:
+        rpi = 12.0 * M * M + k_pi * (16.0 * M * M + 12.0 * M)
+    else:
+        rpi = covariance_flops(M, strip_rows) + k_pi * (8.0 * M * M + 12.0 * M)
+    return (rpi + 8.0 * M * M + 4.0 * M
             + 8.0 * M * (M - 1) + (k_aby + k_abx) * (n / 2.0) * (25.0 * n + 21.0) + 20.0 * n
             + polish + 8.0 * M * M + 8.0 * M + 20.0)
 
 
 def strip_rows_for(M: int, T: int = 100, H: int = 1024, W: int = 1024, sms: int = B200_SMS) -> int | None:
     """S the library's launcher picks for window M on a T×H×W launch (launch_strip: halve from
-    BOS_STRIP_ROWS while fewer than 4 work items per resident warp, down to 2); None when M
-    runs on a kernel that forms R_y per pixel."""
-    if M > STRIP_MAX_M:
-        return None
-    warps_per_sm = 16 if M <= 8 else 12          # strip_warps_per_sm (1-warp CTAs)
+    BOS_STRIP_ROWS while fewer than 4 work items per resident warp, down to 2); None when the
+    launch is too small for S ≥ BOS_STRIP_MIN_ROWS and runs the row / warp kernel."""
+    warps_per_sm = (16 if M <= 8 else (12 if M <= 11 else 8)) if strip_kind(M) == 1 else 8
     row_items = T * H * ((W + 31) // 32)
     S = STRIP_ROWS
     while S > 2 and row_items // S < 4 * warps_per_sm * sms:
         S //= 2
     return S if S >= STRIP_MIN_ROWS else None
+
+
+def path_flops(M: int, k_pi: float, k_aby: float, k_abx: float, T: int, H: int, W: int) -> float:
+    """flops_per_pixel for the kernel the library runs on a T×H×W launch of window M."""
+    S = strip_rows_for(M, T, H, W)
+    if S is None:
+        return flops_per_pixel(M, k_pi, k_aby, k_abx)
+    kind = strip_kind(M)
+    return flops_per_pixel(M, k_pi, k_aby, k_abx, strip_rows=S if kind == 1 else None, kind=kind)
 
 
 class ClockSampler:
@@ -237,7 +256,7 @@ WIDE_MIN_M = 21   # first window on the warp-per-pixel kernel (BOS_WIDE_MIN_M, c
 
 def kernel_name(M: int, T: int = 100, H: int = 1024, W: int = 1024) -> str:
     if strip_rows_for(M, T, H, W):
-        return f"bos::demod_strip_kernel<{M},false>"
+        return f"bos::{'demod_strip_kernel' if strip_kind(M) == 1 else 'demod_strip_im_kernel'}<{M},false>"
     return f"bos::{'demod_kernel' if M < WIDE_MIN_M else 'demod_wide_kernel'}<{M},false,false>"
 
 
@@ -337,7 +356,7 @@ def extra_points(args, dev):
             k = iteration_means(st[1:], M)
             c2.append({"snr_db": snr, "window_len": M, "mpix_s": px / (ms / 1e3) / 1e6,
                        "iters": {"power": k[0], "aberth_y": k[1], "aberth_x": k[2]},
-                       "flops_per_px": flops_per_pixel(M, *k, strip_rows=strip_rows_for(M, 2, 512, 512))})
+                       "flops_per_px": path_flops(M, *k, 2, 512, 512)})
             del tm
         del st
     res["c2_pair_512"] = {"what": "512^2 reference + flow pair (C2), per-step = raw ref + 2-frame stack, 50 steps",
@@ -352,7 +371,7 @@ def extra_points(args, dev):
     tm = StackTimer(st, 15, "recompute", dev)
     ms, kms, _ = tm.run(3, 2)
     k = iteration_means(st[1:5], 15)
-    f = flops_per_pixel(15, *k, strip_rows=strip_rows_for(15))
+    f = path_flops(15, *k, 100, 1024, 1024)
     res["c3_m15"] = {"mpix_s": 100 * 1024 * 1024 * 3 / (ms / 1e3) / 1e6, "kernel": kernel_name(15),
                      "frac_own_model": f * 100 * 1024 * 1024 / (kms / 1e3) / 1e12 / nominal_peak(),
                      "iters": {"power": k[0], "aberth_y": k[1], "aberth_x": k[2]}}
@@ -420,7 +439,7 @@ def run_cuda(args, world, rank, local):
     ms_per_step = elapsed_ms / args.steps
 
     # roofline of the dominant kernel (the T-frame demod launch; the ref launch is 1/T of it)
-    f_px = flops_per_pixel(M, k_pi, k_aby, k_abx, strip_rows=strip_rows_for(M, T, H, W))
+    f_px = path_flops(M, k_pi, k_aby, k_abx, T, H, W)
     achieved = f_px * T * plane / (kern_ms / 1e3) / 1e12
     sm_max = float(peaks().get("sm_max_mhz", 1965.0))
     peak = nominal_peak(sm_max)

@@ -26,8 +26,13 @@
  * Error convention: every entry point returns an int status (BOS_OK or a negative
  * code) and never aborts or exits.  Asynchronous device faults surface at the caller's
  * next synchronisation (CUDA semantics).  bos_strerror() maps a code to a static string.
- * The library keeps no global mutable state: calls are re-entrant and thread-safe across
- * streams.
+ * Calls are re-entrant and thread-safe across streams.  The only global state is the
+ * per-device pair of pipeline streams (+ 4 events) of bos_rootmusic_demod_stack_host,
+ * created on its first use on a device and kept for the life of the process, its enqueue
+ * section serialised by a per-device mutex; and a per-device cache of the strip kernels'
+ * occupancy (read-only after the first launch).  BOS_THREAD_KERNEL=row|strip (environment,
+ * read per launch) forces the paper path's thread-per-pixel kernel for A/B timing; the two
+ * give bitwise identical results.
  */
 #ifndef BOS_ROOTMUSIC_H
 #define BOS_ROOTMUSIC_H
@@ -123,7 +128,8 @@ size_t bos_rootmusic_host_workspace_bytes(int H, int W, int chunk_frames, int wi
  * bos_rootmusic_demod_stack_host — bos_rootmusic_demod_stack on HOST buffers: the frames
  * are streamed host→device in chunks of chunk_frames, demodulated, and the phases (and
  * flags) streamed back, with the copies of one chunk overlapping the kernels of the
- * other on two internal streams (created and destroyed inside the call).
+ * other on two internal streams (created on the first call on a device and reused; see
+ * the file header).
  *   h_frames     HOST [n_frames][H][W] bos_cf32 (pinned for full overlap; pageable works).
  *   h_out_phase  HOST [n_frames][H][W] float32, written.  h_flags: HOST uint8 or NULL.
  *   d_workspace  DEVICE scratch of ≥ bos_rootmusic_host_workspace_bytes(H, W, chunk_frames,
@@ -172,7 +178,11 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W,
  *            rounding bound, Eq.(15) in double; outputs are still float32.  Also sets
  *            BOS_FLAG_SMALL_GAP (λ1/λ2 < 1.3; with FB or smoothing the smaller of the two
  *            axes').  Built for accuracy, not speed (thread-local matrices: ≈50 KB local
- *            memory per thread at M = 32).
+ *            memory per thread at M = 32).  CUDA sizes the local-memory reservation as
+ *            per-thread stack × resident threads per SM × SMs (≈ 16 GB at M = 32 on a B200)
+ *            on the first such launch and keeps it for the context's life: leave that much
+ *            device memory free, or lower it afterwards with cudaDeviceSetLimit(
+ *            cudaLimitStackSize, …) once the call has completed.
  *            Any other bit: BOS_ERR_UNSUPPORTED.
  * The FP32 variants run the hot path's kernels (demod_kernel.cuh, demod_wide.cuh; smoothing:
  * demod_ss.cuh); FP64 runs demod_f64.cuh.  Other arguments, errors and determinism as

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 
 #include "bos_rootmusic.h"
 #include "launch.h"
@@ -195,6 +196,17 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
+// per-device pipeline objects of bos_rootmusic_demod_stack_host (created on first use, kept
+// for the life of the process)
+constexpr int kPipeDevices = 64;
+struct Pipe {
+    bool ready = false;
+    cudaStream_t st[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr, ev_ref = nullptr, ev_end[2] = {nullptr, nullptr};
+};
+Pipe g_pipe[kPipeDevices];
+std::mutex g_pipe_mutex[kPipeDevices];
+
 // Eq.(17): ∂n/∂x = (1/(2 μ f_x)) (n0/L²) φ — a pointwise scale (vectorised, HBM-bound).
 __global__ void index_gradient_kernel(const float* __restrict__ phase, size_t n, float k, float* __restrict__ out) {
     const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -369,19 +381,31 @@ int bos_rootmusic_demod_stack_host(const bos_cf32* h_frames, int n_frames, int H
     }
 
     cudaStream_t user = static_cast<cudaStream_t>(stream);
-    cudaStream_t st[2] = {nullptr, nullptr};
-    cudaEvent_t ev_start = nullptr, ev_ref = nullptr, ev_end[2] = {nullptr, nullptr};
     cudaError_t e = cudaSuccess;
     auto ok = [&](cudaError_t x) {
         if (e == cudaSuccess && x != cudaSuccess) e = x;
         return e == cudaSuccess;
     };
-    ok(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
-    ok(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
-    ok(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-    ok(cudaEventCreateWithFlags(&ev_ref, cudaEventDisableTiming));
-    ok(cudaEventCreateWithFlags(&ev_end[0], cudaEventDisableTiming));
-    ok(cudaEventCreateWithFlags(&ev_end[1], cudaEventDisableTiming));
+    // The two side streams and four events of the pipeline are created once per device and
+    // reused (a call used to create and destroy them: ~tens of µs of driver work per call).
+    // One mutex per device serialises the enqueue section of concurrent calls, so an event is
+    // never re-recorded by another call between its record and the waits on it.
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kPipeDevices) return BOS_ERR_CUDA;
+    std::lock_guard<std::mutex> lock(g_pipe_mutex[dev]);
+    Pipe& pp = g_pipe[dev];
+    if (!pp.ready) {
+        ok(cudaStreamCreateWithFlags(&pp.st[0], cudaStreamNonBlocking));
+        ok(cudaStreamCreateWithFlags(&pp.st[1], cudaStreamNonBlocking));
+        ok(cudaEventCreateWithFlags(&pp.ev_start, cudaEventDisableTiming));
+        ok(cudaEventCreateWithFlags(&pp.ev_ref, cudaEventDisableTiming));
+        ok(cudaEventCreateWithFlags(&pp.ev_end[0], cudaEventDisableTiming));
+        ok(cudaEventCreateWithFlags(&pp.ev_end[1], cudaEventDisableTiming));
+        if (e != cudaSuccess) return BOS_ERR_CUDA;
+        pp.ready = true;
+    }
+    cudaStream_t* st = pp.st;
+    cudaEvent_t ev_start = pp.ev_start, ev_ref = pp.ev_ref, *ev_end = pp.ev_end;
     if (e == cudaSuccess) {
         ok(cudaEventRecord(ev_start, user));
         ok(cudaStreamWaitEvent(st[0], ev_start, 0));
@@ -419,12 +443,6 @@ int bos_rootmusic_demod_stack_host(const bos_cf32* h_frames, int n_frames, int H
         cudaStreamWaitEvent(user, ev_end[0], 0);
         cudaStreamWaitEvent(user, ev_end[1], 0);
     }
-    for (int s = 0; s < 2; ++s) {
-        if (st[s]) cudaStreamDestroy(st[s]);   // deferred until queued work completes
-        if (ev_end[s]) cudaEventDestroy(ev_end[s]);
-    }
-    if (ev_start) cudaEventDestroy(ev_start);
-    if (ev_ref) cudaEventDestroy(ev_ref);
     return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 

@@ -30,14 +30,16 @@ inline int thread_kernel_forced() {
 // Launches too small for S ≥ BOS_STRIP_MIN_ROWS at ≥ 4 items per resident warp return
 // cudaErrorNotReady without launching (a cold start per 2–4 rows costs more than the sliding
 // covariance saves: C2 512² pairs ran 9 % slower) and go to the row kernel.
-template <int M, bool COUNT, bool RS>
+// KIND (strip_kind): 1 = R_y slid in registers (demod_strip_kernel), 2 = no R_y, implicit
+// power iteration (demod_strip_im_kernel)
+template <int M, bool COUNT, int KIND>
 cudaError_t launch_strip(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
-    constexpr int WARPS = RS ? 1 : strip_warps<M>();
-    constexpr size_t smem = RS ? strip_rs_smem_bytes<M>() : strip_smem_bytes<M>();
+    constexpr int WARPS = KIND == 1 ? strip_warps<M>() : 1;
+    constexpr size_t smem = KIND == 1 ? strip_smem_bytes<M>() : strip_im_smem_bytes<M>();
     auto kern = [] {
-        if constexpr (RS) return demod_strip_rs_kernel<M, COUNT>;
+        if constexpr (KIND == 2) return demod_strip_im_kernel<M, COUNT>;
         else return demod_strip_kernel<M, COUNT>;
     }();
     int dev = 0;
@@ -75,12 +77,12 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
     const dim3 block(kBX, kBY, 1);
-    if constexpr (!FB && !COUNT && (M <= kStripMaxM || (M >= kStripRsMinM && M <= kStripRsMaxM))) {
-        // paper path: sliding-covariance strip kernel (R_y in registers up to kStripMaxM, in the
-        // thread's shared-memory slice from kStripRsMinM)
+    constexpr int kKind = strip_kind<M>();
+    if constexpr (!FB && !COUNT && kKind > 0) {
+        // paper path: the strip kernels (demod_strip.cuh); small launches fall through
         if (thread_kernel_forced() != 1) {
-            const cudaError_t e = launch_strip<M, false, (M > kStripMaxM)>(frames, n_frames, H, W, ref, out, flags,
-                                                                            omega_x, omega_y, counters, s);
+            const cudaError_t e =
+                launch_strip<M, false, kKind>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters, s);
             if (e != cudaErrorNotReady) return e;
         }
     }

@@ -816,14 +816,13 @@ __device__ __forceinline__ float roots_and_phase(const float2* win, const cx2 (&
     return a;
 }
 
-// roots_and_phase for the paper path with v_1 = Γ_w^H u_1/‖·‖ formed inside the axis loop when
-// the x axis starts (the strip kernels): only u stays live across the rooting of both axes —
-// with v_1 and a copy of u both live (roots_and_phase) the rolled axis loop carried 4M extra
-// registers through both Aberth runs.  Same arithmetic, bitwise the same result.
-template <int M, int TW, bool FB, bool WEAK_TIGHT = false>
-__device__ __forceinline__ float roots_and_phase_jit(const float2* win, const cx2 (&u)[M], float trace,
-                                                 bool pow_ok, uint8_t& fl, int& n_aby, int& n_abx, float2& zx_out,
-                                                 float2& zy_out) {
+// roots_and_phase with the axis vectors supplied by qfn(axis, q) (axis 0: u_1, axis 1: v_1):
+// the strip kernels form v_1 when the x axis starts (roots_and_phase_jit) or keep both vectors
+// in shared memory (demod_strip_im_kernel), so no second M-vector is carried in registers
+// through both Aberth runs.  Same arithmetic as roots_and_phase.
+template <int M, int TW, bool FB, bool WEAK_TIGHT, class QFn>
+__device__ __forceinline__ float roots_and_phase_q(const float2* win, QFn&& qfn, float trace, bool pow_ok, uint8_t& fl,
+                                                   int& n_aby, int& n_abx, float2& zx_out, float2& zy_out) {
     constexpr int N = 2 * M - 2;
     constexpr int O0 = (M - 1) / 2;
 
@@ -834,12 +833,7 @@ __device__ __forceinline__ float roots_and_phase_jit(const float2* win, const cx
 #pragma unroll 1
     for (int axis = 0; axis < 2; ++axis) {
         float2 q[M];
-        if (axis == 0) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) q[i] = cx2_f2(u[i]);
-        } else {
-            v1_from_window<M, TW>(win, u, q);      // v_1, formed when the x axis needs it
-        }
+        qfn(axis, q);                              // u_1 (axis 0) or v_1 (axis 1), unit norm
         cx2 c[N + 1];
         const float2 rot = music_coeffs<M>(q, c);
         cx2 z[N / 2];       // the inside half of the rotated template
@@ -938,6 +932,27 @@ __device__ __forceinline__ float roots_and_phase_jit(const float2* win, const cx
     zx_out = zx;
     zy_out = zy;
     return a;
+}
+
+// roots_and_phase for the paper path with v_1 = Γ_w^H u_1/‖·‖ formed inside the axis loop when
+// the x axis starts: only u stays live across the rooting of both axes — with v_1 and a copy
+// of u both live (roots_and_phase) the rolled axis loop carried 4M extra registers through
+// both Aberth runs.  Same arithmetic, bitwise the same result.
+template <int M, int TW, bool FB, bool WEAK_TIGHT = false>
+__device__ __forceinline__ float roots_and_phase_jit(const float2* win, const cx2 (&u)[M], float trace,
+                                                     bool pow_ok, uint8_t& fl, int& n_aby, int& n_abx,
+                                                     float2& zx_out, float2& zy_out) {
+    return roots_and_phase_q<M, TW, FB, WEAK_TIGHT>(
+        win,
+        [&](int axis, float2 (&q)[M]) {
+            if (axis == 0) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) q[i] = cx2_f2(u[i]);
+            } else {
+                v1_from_window<M, TW>(win, u, q);      // v_1, formed when the x axis needs it
+            }
+        },
+        trace, pow_ok, fl, n_aby, n_abx, zx_out, zy_out);
 }
 
 // CTAs per SM the register budget is tuned for (no spills at -O3; ptxas -v in the build log).

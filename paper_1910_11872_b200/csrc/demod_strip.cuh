@@ -1,5 +1,5 @@
 // demod_strip.cuh — the paper-path thread-per-pixel kernel with a sliding covariance
-// ("strip kernel", window sizes M ≤ BOS_STRIP_MAX_M).
+// ("strip kernels": R_y slid in registers, or no R_y at all for the larger windows).
 //
 // Same per-pixel chain as demod_kernel.cuh (Algorithm 1: a2 R_y = Γ_wΓ_w^H,
 // a3 power iteration + v_1 = Γ_w^H u_1, a4 coefficients, a5 symmetric Aberth + selection,
@@ -35,15 +35,21 @@
 
 #include "demod_kernel.cuh"
 
-#ifndef BOS_STRIP_MAX_M
-#define BOS_STRIP_MAX_M 14
-#endif
-
 namespace bos {
 
-constexpr int kStripMaxM = BOS_STRIP_MAX_M;
-
-// warps per CTA (shared-memory granularity: the R slices grow as M²) and the register budget
+// Which paper-path kernel runs window M on a large launch (measured per M, round 2, C3 1024²,
+// 10 and 0 dB: profiles/r02_strip.md):  1 = strip kernel with R_y in registers (faster up to
+// M = 10 and at 12, 13);  2 = implicit-power-iteration strip kernel (M = 11 and 14…32: equal
+// at 11 and without the register kernel's 160-byte spill, +1…+130 % from 14);  0 = none (the
+// row kernel).  BOS_STRIP_KIND_OVERRIDE=k forces kind k for every M (A/B builds).
+template <int M>
+constexpr int strip_kind() {
+#ifdef BOS_STRIP_KIND_OVERRIDE
+    return BOS_STRIP_KIND_OVERRIDE;
+#else
+    return (M <= 10 || M == 12 || M == 13) ? 1 : 2;
+#endif
+}
 #ifndef BOS_STRIP_ROWS
 #define BOS_STRIP_ROWS 16        // S: rows per work item (fewer for small launches, see launch_strip)
 #endif
@@ -324,79 +330,58 @@ demod_strip_kernel(const float2* __restrict__ frames, int n_frames, int H, int W
 }
 
 
-// ---- Larger windows (BOS_STRIP_RS_MIN_M ≤ M ≤ BOS_STRIP_RS_MAX_M): R_y never fits the registers
-// beside the rooting state, so it lives in the thread's shared-memory slice for good (as the row
-// kernel's kRsmem path): full at the strip start, then shifted in place (ascending entry order:
-// every source is read before any later write reaches it) plus the new last row, and the power
-// iteration reads it from there.  Order of the power-iteration sums: the row kernel's for the
-// same M (registers below BOS_RSMEM_MIN_M, power_iteration_smem from it), so the outputs stay
-// bitwise the row kernel's.
-#ifndef BOS_STRIP_RS_MIN_M
-#define BOS_STRIP_RS_MIN_M 16
-#endif
-#ifndef BOS_STRIP_RS_MAX_M
-#define BOS_STRIP_RS_MAX_M 22
-#endif
-constexpr int kStripWeakTightMinM = kWeakTightMinM;     // demod_kernel.cuh
-constexpr int kStripRsMinM = BOS_STRIP_RS_MIN_M;
-constexpr int kStripRsMaxM = BOS_STRIP_RS_MAX_M;
+// ---- Larger windows (strip_kind<M>() == 2): no R_y at all.  From M ≈ 11 R_y no longer fits
+// the registers beside the rooting state (the row kernel spills 0.1–2.4 KB per thread at
+// M = 11…20), and a per-thread shared-memory copy of it (M(M−1)/2 entries, slid in place — an
+// intermediate version) limits a B200 SM to 6…2 warps at M = 15…24.  Here the power iteration
+// applies R_y = Γ_wΓ_w^H as Γ_w(Γ_w^H u) straight from the window tile (2M² instead of M²
+// complex MACs per iteration, no M³/2 build, no slide), the
+// trace and the lag-1 sum Σ_i R[i+1][i] come from one pass over the window, and u_1, v_1 wait
+// in the thread's shared-memory slice while the other axis is rooted.  The loops over the
+// window run rolled over one index (loop-carried vectors go through the slice), which keeps
+// the kernel's code — and its instruction-cache footprint — O(M) instead of O(M²).
+// Same FP32 chain otherwise; parity against the FP64 oracle (tests/test_gpu_strip.py).
 
 template <int M>
-constexpr size_t strip_rs_smem_bytes() {      // one warp per CTA
-    return (size_t)(M + 1) * (32 + M - 1) * sizeof(float2) + (size_t)32 * (M * (M - 1) / 2) * sizeof(cx2) +
-           (size_t)32 * M * sizeof(float);
-}
-template <int M>
-constexpr int strip_rs_min_blocks() {         // what the shared memory admits (≈ 227 KB per SM), ≤ 8 (255 registers)
-    constexpr int b = (int)(227 * 1024 / (strip_rs_smem_bytes<M>() + 1024));
-    return b < 1 ? 1 : (b > 8 ? 8 : b);
+constexpr size_t strip_im_smem_bytes() {      // one warp: tile (M+1 rows) + 2 M-vectors per lane
+    return (size_t)(M + 1) * (32 + M - 1) * sizeof(float2) + (size_t)32 * 2 * M * sizeof(cx2);
 }
 
-// row I of R_y (entries (I, j), j < I, and the diagonal I) over the window, to the slice
-template <int M, int TW, int I>
-__device__ __forceinline__ void strip_rs_row(const float2* win, cx2* Rs, float* Rds) {
-    constexpr int B = I * (I - 1) / 2;
-    cx2 acc[I > 0 ? I : 1];
-    float d = 0.0f;
+// t = Γ_w^H u column by column (t_k = Σ_i conj(Γ(i,k)) u_i, v1_from_window's arithmetic) into
+// the slice T (entry k at T[k·32]); returns ‖t‖²
+template <int M, int TW>
+__device__ __forceinline__ float im_gamma_h(const float2* win, const cx2 (&u)[M], cx2* T) {
+    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+    cx2 unj[M];
 #pragma unroll
-    for (int j = 0; j < I; ++j) acc[j] = 0ull;
+    for (int i = 0; i < M; ++i) unj[i] = mul2(cx2_make(cx2_im(u[i]), cx2_re(u[i])), kPosNeg);   // −j·u_i
+    float n2 = 0.0f;
 #pragma unroll 1
     for (int k = 0; k < M; ++k) {
-        const float2 gi = win[I * TW + k];
-        d = fmaf(gi.x, gi.x, fmaf(gi.y, gi.y, d));
-        const cx2 ci = cx2_make(gi.x, gi.y);
-        const cx2 cnj = mul2(cx2_make(gi.y, gi.x), cx2_make(1.0f, -1.0f));
+        cx2 acc = 0ull;
 #pragma unroll
-        for (int j = 0; j < I; ++j) {
-            const float2 gj = win[j * TW + k];
-            acc[j] = fma2(cx2_bcast(gj.x), ci, fma2(cx2_bcast(gj.y), cnj, acc[j]));
+        for (int i = 0; i < M; ++i) {
+            const float2 g = win[i * TW + k];
+            acc = fma2(cx2_bcast(g.x), u[i], fma2(cx2_bcast(g.y), unj[i], acc));
         }
+        T[k * 32] = acc;
+        n2 += cabs2(cx2_f2(acc));
     }
-#pragma unroll
-    for (int j = 0; j < I; ++j) Rs[(B + j) * 32] = acc[j];
-    Rds[I * 32] = d;
-}
-template <int M, int TW, int I = 0>
-__device__ __forceinline__ void strip_rs_all(const float2* win, cx2* Rs, float* Rds) {
-    if constexpr (I < M) {
-        strip_rs_row<M, TW, I>(win, Rs, Rds);
-        strip_rs_all<M, TW, I + 1>(win, Rs, Rds);
-    }
+    return n2;
 }
 
 template <int M, bool COUNT>
-__global__ void __launch_bounds__(32, strip_rs_min_blocks<M>())
-demod_strip_rs_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int S,
+__global__ void __launch_bounds__(32, 8)
+demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int S,
                       const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
                       float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
     constexpr int O0 = (M - 1) / 2;
     constexpr int TW = kBX + M - 1;
-    constexpr int NOFF = M * (M - 1) / 2;
     extern __shared__ __align__(16) unsigned char strip_smem[];
     const int lane = threadIdx.x;
     float2* tile = reinterpret_cast<float2*>(strip_smem);
-    cx2* Rs = reinterpret_cast<cx2*>(tile + (M + 1) * TW) + lane;           // entry t at Rs[t·32]
-    float* Rds = reinterpret_cast<float*>(reinterpret_cast<cx2*>(tile + (M + 1) * TW) + NOFF * 32) + lane;
+    cx2* Us = reinterpret_cast<cx2*>(tile + (M + 1) * TW) + lane;   // u_1: entry i at Us[i·32]
+    cx2* Vs = Us + M * 32;                                         // v_1 (and the iteration's scratch)
     const size_t plane = (size_t)H * (size_t)W;
     const int nbx = (W + kBX - 1) / kBX;
     const int nstrip = (H + S - 1) / S;
@@ -441,26 +426,28 @@ demod_strip_rs_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                 uint8_t fl = 0;
                 if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
                     fl |= kFlagBorder;
-                // ---- a2: R_y in the slice: in full at the strip start, else shift + new last row ----
-                if (s == 0) {
-                    strip_rs_all<M, TW>(win, Rs, Rds);
-                } else {
-#pragma unroll
-                    for (int i = 0; i + 1 < M; ++i) Rds[i * 32] = Rds[(i + 1) * 32];
-#pragma unroll
-                    for (int i = 1; i + 1 < M; ++i) {
-                        compiler_fence();           // row by row (see compiler_fence)
-#pragma unroll
-                        for (int j = 0; j < i; ++j) Rs[tri_off<M>(i, j) * 32] = Rs[tri_off<M>(i + 1, j + 1) * 32];
-                    }
-                    strip_rs_row<M, TW, M - 1>(win, Rs, Rds);
-                }
-                float Rd[M];
+                // ---- tr R_y = ‖Γ_w‖_F² and r1 = Σ_i R[i+1][i] = Σ_k Σ_i Γ(i+1,k) conj(Γ(i,k)), one pass ----
                 float trace = 0.0f;
+                float2 r1 = make_float2(0.0f, 0.0f);
+                {
+                    float2 prev[M];
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    Rd[i] = Rds[i * 32];
-                    trace += Rd[i];
+                    for (int k = 0; k < M; ++k) {
+                        prev[k] = win[k];
+                        trace = fmaf(prev[k].x, prev[k].x, fmaf(prev[k].y, prev[k].y, trace));
+                    }
+#pragma unroll 1
+                    for (int i = 1; i < M; ++i) {
+                        float2 racc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                        for (int k = 0; k < M; ++k) {
+                            const float2 g = win[i * TW + k];
+                            trace = fmaf(g.x, g.x, fmaf(g.y, g.y, trace));
+                            racc = cfmac(g, prev[k], racc);            // g · conj(prev)
+                            prev[k] = g;
+                        }
+                        r1 = cadd(r1, racc);
+                    }
                 }
                 float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
                 int n_pow = 0, n_aby = 0, n_abx = 0;
@@ -468,70 +455,78 @@ demod_strip_rs_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                     fl |= kFlagNonfinite;
                     result = CUDART_NAN_F;
                 } else {
+                    // ---- a3: power iteration y = Γ_w(Γ_w^H u) from the lag-1 tone start ----
                     cx2 u[M];
-                    bool pow_ok = false;
-                    float lam2 = CUDART_INF_F;          // ‖R u‖² at convergence (row-order branch)
-                    if constexpr (M >= BOS_RSMEM_MIN_M) {
-                        n_pow = power_iteration_smem<M, 32, true>(Rd, Rs, u, pow_ok, &lam2);
-                    } else {
-                        // the row kernel's register order, R read from the slice (entries twice)
-                        float2 r1 = make_float2(0.0f, 0.0f);
-#pragma unroll
-                        for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Rs[tri_off<M>(i + 1, i) * 32]));
+                    {
                         float2 e = make_float2(1.0f, 0.0f);
                         if (cabs2(r1) > 0.0f) e = cscale(r1, rsqrtf(cabs2(r1)));
-                        {
-                            float2 t = make_float2(rsqrtf(float(M)), 0.0f);
+                        float2 t = make_float2(rsqrtf(float(M)), 0.0f);
 #pragma unroll
-                            for (int i = 0; i < M; ++i) {
-                                u[i] = cx2_make(t.x, t.y);
-                                t = cmul(t, e);
-                            }
-                        }
-                        for (n_pow = 0; n_pow < kPowerMaxIt;) {
-                            cx2 uj[M];
-#pragma unroll
-                            for (int j = 0; j < M; ++j) uj[j] = mul2(cx2_make(cx2_im(u[j]), cx2_re(u[j])), cx2_make(-1.0f, 1.0f));
-                            cx2 y[M];
-#pragma unroll
-                            for (int i = 0; i < M; ++i) {
-                                compiler_fence();
-                                cx2 acc = mul2(cx2_bcast(Rd[i]), u[i]);
-#pragma unroll
-                                for (int j = 0; j < i; ++j) {
-                                    const cx2 r = Rs[tri_off<M>(i, j) * 32];
-                                    acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(cx2_im(r)), uj[j], acc));
-                                }
-#pragma unroll
-                                for (int j = i + 1; j < M; ++j) {
-                                    const cx2 r = Rs[tri_off<M>(j, i) * 32];
-                                    acc = fma2(cx2_bcast(cx2_re(r)), u[j], fma2(cx2_bcast(-cx2_im(r)), uj[j], acc));
-                                }
-                                y[i] = acc;
-                            }
-                            float nrm2 = 0.0f;
-#pragma unroll
-                            for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
-                            const cx2 inv = cx2_bcast(rsqrtf(nrm2));
-                            float diff = 0.0f;
-#pragma unroll
-                            for (int i = 0; i < M; ++i) {
-                                const cx2 yn = mul2(y[i], inv);
-                                diff += cabs2(cx2_f2(sub2(yn, u[i])));
-                                u[i] = yn;
-                            }
-                            ++n_pow;
-                            if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
+                        for (int i = 0; i < M; ++i) {
+                            u[i] = cx2_make(t.x, t.y);
+                            t = cmul(t, e);
                         }
                     }
-                    if constexpr (!newton_stop<false, M>()) {   // weak-tone window (demod_kernel.cuh, newton_stop)
-                        if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
-                    } else if constexpr (M >= kStripWeakTightMinM) {   // the warp kernel's weak-tone rule
+                    bool pow_ok = false;
+                    float lam2 = CUDART_INF_F;
+                    for (n_pow = 0; n_pow < kPowerMaxIt;) {
+                        im_gamma_h<M, TW>(win, u, Vs);                 // t = Γ^H u → slice
+                        cx2 t[M], tj[M];
+#pragma unroll
+                        for (int k = 0; k < M; ++k) {
+                            t[k] = Vs[k * 32];
+                            tj[k] = mul2(cx2_make(cx2_im(t[k]), cx2_re(t[k])), cx2_make(-1.0f, 1.0f));   // j·t
+                        }
+                        // y_i = Σ_k Γ(i,k) t_k, row by row → slice
+#pragma unroll 1
+                        for (int i = 0; i < M; ++i) {
+                            cx2 acc = 0ull;
+#pragma unroll
+                            for (int k = 0; k < M; ++k) {
+                                const float2 g = win[i * TW + k];
+                                acc = fma2(cx2_bcast(g.x), t[k], fma2(cx2_bcast(g.y), tj[k], acc));
+                            }
+                            Vs[i * 32] = acc;
+                        }
+                        cx2 y[M];
+                        float nrm2 = 0.0f;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            y[i] = Vs[i * 32];
+                            nrm2 += cabs2(cx2_f2(y[i]));
+                        }
+                        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+                        float diff = 0.0f;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) {
+                            const cx2 yn = mul2(y[i], inv);
+                            diff += cabs2(cx2_f2(sub2(yn, u[i])));
+                            u[i] = yn;
+                        }
+                        ++n_pow;
+                        if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
+                    }
+                    if constexpr (M >= kWeakTightMinM)
                         if (lam2 < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
+                    // u_1 and v_1 = Γ_w^H u_1/‖·‖ to the slice (v1_from_window's arithmetic)
+                    {
+                        const float vn = im_gamma_h<M, TW>(win, u, Vs);
+                        const cx2 vinv = cx2_bcast(rsqrtf(vn));
+#pragma unroll
+                        for (int k = 0; k < M; ++k) {
+                            Vs[k * 32] = mul2(Vs[k * 32], vinv);
+                            Us[k * 32] = u[k];
+                        }
                     }
                     float2 zx, zy;
-                    float a = roots_and_phase_jit<M, TW, false, (M >= kStripWeakTightMinM)>(win, u, trace, pow_ok, fl,
-                                                                                            n_aby, n_abx, zx, zy);
+                    float a = roots_and_phase_q<M, TW, false, (M >= kWeakTightMinM)>(
+                        win,
+                        [&](int axis, float2 (&q)[M]) {
+                            const cx2* Q = axis ? Vs : Us;
+#pragma unroll
+                            for (int i = 0; i < M; ++i) q[i] = cx2_f2(Q[i * 32]);
+                        },
+                        trace, pow_ok, fl, n_aby, n_abx, zx, zy);
                     if (omx != nullptr) wx = -atan2f(zx.y, zx.x);
                     if (omy != nullptr) wy = atan2f(zy.y, zy.x);
                     if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);

@@ -24,9 +24,11 @@
 
 namespace bos {
 
-// Smallest window handled warp-per-pixel.  The thread kernel keeps R_y in shared memory for
-// M = 17…20 (kRsmem) and beats this kernel there (M = 19: 200 vs 154, M = 20: 166 vs 147
-// Mpixel/s); the FB variant (registers only) switches at 19.
+// Smallest window handled warp-per-pixel by the row-kernel dispatch (small launches of the
+// paper path and the FB variant; FB switches at 19).  Large paper-path launches of M ≤ 22 run
+// the strip kernels (demod_strip.cuh) instead: round-2 C3 1024² ×8, 10 dB: M = 21 286 vs 156,
+// M = 22 260 vs 149 Mpixel/s (profiles/r02_c4_sweep.md); from M = 23 this kernel is faster
+// (the strip kernel's shared-memory R_y leaves 2 warps per SM).
 #ifndef BOS_WIDE_MIN_M
 #define BOS_WIDE_MIN_M 21
 #endif

@@ -83,7 +83,7 @@ def main():
             cnt = bosrm.bos_rootmusic_iteration_counts(frames[1:2], M)
             npx = cnt["pixels"]
             kpi, ky, kx = cnt["power_its"] / npx, cnt["aberth_y"] / npx, cnt["aberth_x"] / npx
-            fpx = bench.flops_per_pixel(M, kpi, ky, kx, strip_rows=bench.strip_rows_for(M, T, w.H, w.W))
+            fpx = bench.path_flops(M, kpi, ky, kx, T, w.H, w.W)
         tf = fpx * mpx * 1e6 / 1e12
         rng = np.random.default_rng(M)
         pix = (rng.integers(0, w.H, args.parity_px), rng.integers(0, w.W, args.parity_px))
@@ -96,7 +96,7 @@ def main():
         rms, mx = float(math.sqrt(np.mean(e * e))), float(np.max(np.abs(e)))
         row = dict(M=M, variant=args.variant, subarray=sub_of(M), mpix_s=mpx, fps_2048=mpx / (plane / 1e6), power_its=kpi, aberth_y=ky, aberth_x=kx,
                    kflop_px=fpx / 1e3, tflops=tf, frac=tf / peak, parity_rms=rms, parity_max=mx,
-                   kernel="demod_kernel (thread/pixel)" if M <= 20 else "demod_wide_kernel (warp/pixel)")
+                   kernel=bench.kernel_name(M, T, w.H, w.W) if not fb else "variant")
         rows.append(row)
         print(f"| {M} | {mpx:.1f} | {row['fps_2048']:.1f} | {kpi:.2f} | {ky:.2f}/{kx:.2f} | {fpx / 1e3:.1f} | "
               f"{tf:.1f} | {tf / peak:.3f} | {rms:.1e} / {mx:.1e} |", flush=True)
