@@ -370,8 +370,16 @@ __device__ __forceinline__ float im_gamma_h(const float2* win, const cx2 (&u)[M]
     return n2;
 }
 
+// resident warps per SM the implicit kernel's register budget is sized for (12 → ≤ 168
+// registers, 8 → ≤ 255); BOS_STRIP_IM_WARPS_MAX_M12 = the largest M given 12
+#ifndef BOS_STRIP_IM_WARPS_MAX_M12
+#define BOS_STRIP_IM_WARPS_MAX_M12 18   // measured: M = 15, 16 +6 %, 17 +3 %, 18 +2 %; M = 20 −4 % (shared memory caps it at 11 warps)
+#endif
+template <int M>
+constexpr int strip_im_min_blocks() { return M <= BOS_STRIP_IM_WARPS_MAX_M12 ? 12 : 8; }
+
 template <int M, bool COUNT>
-__global__ void __launch_bounds__(32, 8)
+__global__ void __launch_bounds__(32, strip_im_min_blocks<M>())
 demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int S,
                       const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
                       float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
