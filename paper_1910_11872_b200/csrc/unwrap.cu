@@ -12,7 +12,9 @@
 // chosen neighbour's root with the offset that satisfies the edge, and pointer jumping sums
 // offsets to the root.  The reliabilities are computed in FP64 with the oracle's operation
 // order and IEEE round-to-nearest intrinsics, so the edge order — and hence every 2π multiple —
-// is identical to the FP64 oracle (oracle/unwrap.py).
+// is identical to the FP64 oracle (oracle/unwrap.py).  After every round the edges that still
+// cross components are compacted (order-preserving) into a list, so later rounds touch only
+// those: round 0 scans all 2·H·W edges, later rounds a shrinking fraction.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -83,40 +85,253 @@ __device__ __forceinline__ bool edge_ends(unsigned e, int H, int W, int& p, int&
 }
 
 // pass 1: every component's largest incident cross-edge reliability (positive doubles order as u64)
+__device__ __forceinline__ void edge_max_one(unsigned e, int H, int W, const double* __restrict__ rel,
+                                             const unsigned long long* __restrict__ po, unsigned long long* best_rel) {
+    int p, q;
+    if (!edge_ends(e, H, W, p, q)) return;
+    const int rp = par(po[p]), rq = par(po[q]);
+    if (rp == rq) return;
+    const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
+    atomicMax(best_rel + rp, key);
+    atomicMax(best_rel + rq, key);
+}
+// pass 2: among the edges at that reliability, the smallest id
+__device__ __forceinline__ void edge_argmin_one(unsigned e, int H, int W, const double* __restrict__ rel,
+                                                const unsigned long long* __restrict__ po,
+                                                const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
+    int p, q;
+    if (!edge_ends(e, H, W, p, q)) return;
+    const int rp = par(po[p]), rq = par(po[q]);
+    if (rp == rq) return;
+    const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
+    if (key == best_rel[rp]) atomicMin(best_id + rp, e);
+    if (key == best_rel[rq]) atomicMin(best_id + rq, e);
+}
+// round 0: every edge id 0 … 2·H·W·F − 1 (border ids drop out in edge_ends)
 __global__ void edge_max(int H, int W, int F, const double* __restrict__ rel,
                          const unsigned long long* __restrict__ po, unsigned long long* best_rel) {
     const size_t ne = 2 * (size_t)H * W * F;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x) {
-        int p, q;
-        if (!edge_ends((unsigned)e, H, W, p, q)) continue;
-        const int rp = par(po[p]), rq = par(po[q]);
-        if (rp == rq) continue;
-        const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
-        atomicMax(best_rel + rp, key);
-        atomicMax(best_rel + rq, key);
-    }
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x)
+        edge_max_one((unsigned)e, H, W, rel, po, best_rel);
 }
-
-// pass 2: among the edges at that reliability, the smallest id
 __global__ void edge_argmin(int H, int W, int F, const double* __restrict__ rel,
                             const unsigned long long* __restrict__ po,
                             const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
     const size_t ne = 2 * (size_t)H * W * F;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x) {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x)
+        edge_argmin_one((unsigned)e, H, W, rel, po, best_rel, best_id);
+}
+// later rounds: only the edges that still cross components (the compacted list)
+__global__ void edge_max_list(const unsigned* __restrict__ list, unsigned n, int H, int W,
+                              const double* __restrict__ rel, const unsigned long long* __restrict__ po,
+                              unsigned long long* best_rel) {
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        edge_max_one(list[k], H, W, rel, po, best_rel);
+}
+__global__ void edge_argmin_list(const unsigned* __restrict__ list, unsigned n, int H, int W,
+                                 const double* __restrict__ rel, const unsigned long long* __restrict__ po,
+                                 const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        edge_argmin_one(list[k], H, W, rel, po, best_rel, best_id);
+}
+
+// ---- crossing-edge compaction: after a round's re-link every node points at its final root,
+// so an edge is still needed iff its ends have different roots.  Order-preserving stream
+// compaction (count → scan → scatter) keeps the list in edge-id order, hence the memory
+// locality of the next round's passes (an atomically appended list lost it: 57.7 ms vs 44.6).
+constexpr int kFiltThreads = 256;
+constexpr int kFiltPerThread = 8;                              // one flag byte per thread
+constexpr int kFiltPerBlock = kFiltThreads * kFiltPerThread;
+
+template <bool IMPLICIT>
+__device__ __forceinline__ unsigned crossing_bits(const unsigned* __restrict__ list, unsigned n_in, int H, int W,
+                                                  const unsigned long long* __restrict__ po, unsigned base) {
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < kFiltPerThread; ++j) {
+        const unsigned idx = base + j;
+        if (idx >= n_in) break;
+        const unsigned e = IMPLICIT ? idx : list[idx];
         int p, q;
-        if (!edge_ends((unsigned)e, H, W, p, q)) continue;
-        const int rp = par(po[p]), rq = par(po[q]);
-        if (rp == rq) continue;
-        const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
-        if (key == best_rel[rp]) atomicMin(best_id + rp, (unsigned)e);
-        if (key == best_rel[rq]) atomicMin(best_id + rq, (unsigned)e);
+        if (edge_ends(e, H, W, p, q) && par(po[p]) != par(po[q])) m |= 1u << j;
     }
+    return m;
+}
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total) {
+    __shared__ unsigned wsum[kFiltThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned y = lane < kFiltThreads / 32 ? wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += t;
+        }
+        if (lane < kFiltThreads / 32) wsum[lane] = y;        // inclusive warp-sum prefix
+    }
+    __syncthreads();
+    const unsigned before = (w > 0 ? wsum[w - 1] : 0u) + x - v;
+    if (total != nullptr) *total = wsum[kFiltThreads / 32 - 1];
+    return before;
+}
+template <bool IMPLICIT>
+__global__ void __launch_bounds__(kFiltThreads) filter_count(const unsigned* __restrict__ list, unsigned n_in, int H,
+                                                              int W, const unsigned long long* __restrict__ po,
+                                                              uint8_t* __restrict__ bits, unsigned* __restrict__ bcount) {
+    const unsigned t = blockIdx.x * kFiltThreads + threadIdx.x;
+    const unsigned m = crossing_bits<IMPLICIT>(list, n_in, H, W, po, t * kFiltPerThread);
+    bits[t] = (uint8_t)m;
+    unsigned tot;
+    block_excl_scan((unsigned)__popc(m), &tot);
+    if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+}
+// exclusive scan of the per-block counts (one CTA; nb ≤ 2^32 / 2048), total → *count
+__global__ void __launch_bounds__(kFiltThreads) scan_counts(const unsigned* __restrict__ bcount, unsigned nb,
+                                                             unsigned* __restrict__ boff, unsigned* __restrict__ count) {
+    const unsigned per = (nb + kFiltThreads - 1) / kFiltThreads;
+    const unsigned lo = threadIdx.x * per, hi = min(nb, lo + per);
+    unsigned sum = 0;
+    for (unsigned i = lo; i < hi; ++i) sum += bcount[i];
+    unsigned tot;
+    unsigned run = block_excl_scan(sum, &tot);
+    for (unsigned i = lo; i < hi; ++i) {
+        boff[i] = run;
+        run += bcount[i];
+    }
+    if (threadIdx.x == 0) *count = tot;
+}
+template <bool IMPLICIT>
+__global__ void __launch_bounds__(kFiltThreads) filter_scatter(const unsigned* __restrict__ list, unsigned n_in,
+                                                                const uint8_t* __restrict__ bits,
+                                                                const unsigned* __restrict__ boff,
+                                                                unsigned* __restrict__ out) {
+    const unsigned t = blockIdx.x * kFiltThreads + threadIdx.x;
+    const unsigned m = bits[t];
+    unsigned pos = boff[blockIdx.x] + block_excl_scan((unsigned)__popc(m), nullptr);
+    const unsigned base = t * kFiltPerThread;
+#pragma unroll
+    for (int j = 0; j < kFiltPerThread; ++j)
+        if ((m >> j) & 1u) out[pos++] = IMPLICIT ? base + j : list[base + j];
 }
 
 // e(a→b) = (γ(w_b − w_a) − (w_b − w_a)) / 2π  ∈ {−1, 0, 1}: required k(b) − k(a)
 __device__ __forceinline__ int edge_k(const float* __restrict__ w, int a, int b) {
     const double dw = __dsub_rn(fin(w[b]), fin(w[a]));
     return (int)rint(__ddiv_rn(__dsub_rn(gam(dw), dw), 6.283185307179586));
+}
+
+// ---- Phase 1: Borůvka inside kTile×kTile tiles, in shared memory.  A component may contract along
+// its best incident edge only if that edge is the best among ALL its incident edges (cut
+// property of the unique maximum spanning tree), so every node also sees its cross-tile edges
+// (reliabilities of the 1-pixel halo) — a component whose best edge leaves the tile stops
+// growing here and is finished by the global rounds.  Every contracted edge is therefore a
+// global MST edge, and the 2π offsets integrate along the same tree: the result is identical.
+// In smooth regions most best edges are local, so the global rounds start from ~tile-sized
+// components instead of single pixels (their pointer-jumping and re-link passes over all
+// nodes dominated: 13.5 of 38.8 ms per 100 1024² frames in jump_list alone).
+#ifndef BOS_UNWRAP_TILE
+#define BOS_UNWRAP_TILE 16
+#endif
+constexpr int kTile = BOS_UNWRAP_TILE;       // 16: 256-thread CTAs, 8 per SM (32: one 1024-thread CTA per SM — its barriers stall the SM — 14.2 ms of 23.8 per 100 1024² frames)
+__device__ __forceinline__ unsigned tpk(int parent, int off) { return (unsigned)(parent & 0xffff) | ((unsigned)off << 16); }
+__device__ __forceinline__ int tpar(unsigned v) { return (int)(v & 0xffffu); }
+__device__ __forceinline__ int tofs(unsigned v) { return (int)v >> 16; }
+
+__global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_boruvka(const float* __restrict__ w, const double* __restrict__ rel,
+                                                              int H, int W, int F, unsigned long long* __restrict__ po) {
+    __shared__ unsigned node[kTile * kTile];                 // (local parent, 2π offset to it)
+    __shared__ unsigned long long bkey[kTile * kTile];       // best incident key per component root
+    __shared__ unsigned bid[kTile * kTile];                  // best incident edge id per component root
+    __shared__ unsigned staged[kTile * kTile];
+    const int tilesx = (W + kTile - 1) / kTile, tilesy = (H + kTile - 1) / kTile;
+    const int f = blockIdx.x / (tilesx * tilesy);
+    const int t = blockIdx.x % (tilesx * tilesy);
+    const int x0 = (t % tilesx) * kTile, y0 = (t / tilesx) * kTile;
+    const int l = threadIdx.x, lx = l % kTile, ly = l / kTile;
+    const int x = x0 + lx, y = y0 + ly;
+    const bool valid = x < W && y < H;
+    const size_t plane = (size_t)H * W;
+    const int p = (int)((size_t)f * plane + (size_t)y * W + x);
+    node[l] = tpk(l, 0);
+    // this node's 4 incident edges in fixed slots (right, down, left, up): edge id, local index
+    // of the other end (−1: outside the tile), key; `has` = the slots that exist
+    unsigned eid[4] = {0u, 0u, 0u, 0u};
+    int ol[4] = {-1, -1, -1, -1};
+    unsigned long long key[4] = {0ull, 0ull, 0ull, 0ull};
+    unsigned has = 0;
+    if (valid) {
+        const double rp = rel[p];
+        if (x + 1 < W) { has |= 1u; eid[0] = 2u * (unsigned)p;            ol[0] = lx + 1 < kTile ? l + 1 : -1;     key[0] = (unsigned long long)__double_as_longlong(__dadd_rn(rp, rel[p + 1])); }
+        if (y + 1 < H) { has |= 2u; eid[1] = 2u * (unsigned)p + 1u;       ol[1] = ly + 1 < kTile ? l + kTile : -1; key[1] = (unsigned long long)__double_as_longlong(__dadd_rn(rp, rel[p + W])); }
+        if (x > 0)     { has |= 4u; eid[2] = 2u * (unsigned)(p - 1);      ol[2] = lx > 0 ? l - 1 : -1;             key[2] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - 1], rp)); }
+        if (y > 0)     { has |= 8u; eid[3] = 2u * (unsigned)(p - W) + 1u; ol[3] = ly > 0 ? l - kTile : -1;         key[3] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - W], rp)); }
+    }
+    __syncthreads();
+    for (int round = 0; round < 32; ++round) {
+        const int r = tpar(node[l]);                        // fully compressed: the root
+        bkey[l] = 0ull;
+        bid[l] = 0xffffffffu;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (((has >> k) & 1u) && (ol[k] < 0 || tpar(node[ol[k]]) != r)) atomicMax(bkey + r, key[k]);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (((has >> k) & 1u) && (ol[k] < 0 || tpar(node[ol[k]]) != r) && key[k] == bkey[r]) atomicMin(bid + r, eid[k]);
+        __syncthreads();
+        // roots hook across their best edge when it stays inside the tile; the edge's tile-side
+        // end that belongs to this component is p_in, the other end q_out
+        unsigned out = node[l];
+        if (valid && r == l && bid[l] != 0xffffffffu) {
+            const unsigned e = bid[l];
+            const int a = (int)(e >> 1), b = (e & 1u) ? a + W : a + 1;   // global ends
+            const int la = (a - (int)((size_t)f * plane)) / W - y0, ca = (a - (int)((size_t)f * plane)) % W - x0;
+            const int lb = (b - (int)((size_t)f * plane)) / W - y0, cb = (b - (int)((size_t)f * plane)) % W - x0;
+            const bool ain = la >= 0 && la < kTile && ca >= 0 && ca < kTile;
+            const bool bin = lb >= 0 && lb < kTile && cb >= 0 && cb < kTile;
+            if (ain && bin) {
+                const int lA = la * kTile + ca, lB = lb * kTile + cb;
+                const bool aMine = tpar(node[lA]) == l;
+                const int lin = aMine ? lA : lB, lot = aMine ? lB : lA;
+                const int gin = aMine ? a : b, got = aMine ? b : a;
+                const unsigned wo = node[lot], wc = node[lin];
+                const int d = tpar(wo);
+                const bool mutual = bid[d] == e;
+                if (!(mutual && d < l)) {
+                    out = tpk(d, tofs(wo) - tofs(wc) - edge_k(w, gin, got));
+                }
+            }
+        }
+        staged[l] = out;
+        const bool hooked = __syncthreads_or(out != node[l]);
+        if (r == l) node[l] = staged[l];
+        __syncthreads();
+        if (!hooked) break;
+        // pointer jumping to full compression (in place, packed words stay consistent); ends
+        // after a pass in which nothing changed
+        for (int j = 0; j < 12; ++j) {
+            const unsigned v = node[l];
+            const unsigned vp = node[tpar(v)];
+            const bool ch = tpar(vp) != tpar(v);
+            if (ch) node[l] = tpk(tpar(vp), tofs(v) + tofs(vp));
+            if (!__syncthreads_or(ch)) break;
+        }
+    }
+    if (valid) {
+        const unsigned v = node[l];
+        const int rl = tpar(v);
+        const int gr = (int)((size_t)f * plane + (size_t)(y0 + rl / kTile) * W + (x0 + rl % kTile));
+        po[p] = pk(gr, tofs(v));
+    }
 }
 
 // ---- root lists: after the first rounds most nodes are not roots, so the per-round work that
@@ -278,9 +493,12 @@ struct Ws {
     unsigned *list, *list2;           // current roots / next round's roots
     unsigned long long* best_rel;
     unsigned* best_id;
-    int* flags;                  // [0] hooked, [1] changed, [2] scratch, [4] / [5] list counts
+    int* flags;                  // [0] hooked, [1] changed, [2] scratch, [4] / [5] list counts, [6] edge count
     unsigned long long* amax;
     unsigned* aidx;
+    unsigned *edges, *edges2;    // crossing-edge lists (ping-pong), ≤ 2n ids each
+    uint8_t* ebits;              // filter flags, one byte per 8 edges
+    unsigned *bcount, *boff;     // filter per-block counts / offsets
 };
 
 size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
@@ -299,6 +517,12 @@ size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
     char* fl = take(8 * sizeof(int));
     char* am = take(F * sizeof(unsigned long long));
     char* ai = take(F * sizeof(unsigned));
+    const size_t nblk = (2 * n + kFiltPerBlock - 1) / kFiltPerBlock;
+    char* e1 = take(2 * n * sizeof(unsigned));
+    char* e2 = take(2 * n * sizeof(unsigned));
+    char* eb = take(nblk * kFiltThreads);
+    char* bc = take(nblk * sizeof(unsigned));
+    char* bo = take(nblk * sizeof(unsigned));
     if (ws) {
         ws->rel = (double*)r;
         ws->po = (unsigned long long*)p1;
@@ -309,6 +533,11 @@ size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
         ws->flags = (int*)fl;
         ws->amax = (unsigned long long*)am;
         ws->aidx = (unsigned*)ai;
+        ws->edges = (unsigned*)e1;
+        ws->edges2 = (unsigned*)e2;
+        ws->ebits = (uint8_t*)eb;
+        ws->bcount = (unsigned*)bc;
+        ws->boff = (unsigned*)bo;
     }
     return o;
 }
@@ -360,14 +589,30 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
         const float* w = wrapped + (size_t)f0 * plane;
         float* out = unwrapped + (size_t)f0 * plane;
         reliability_kernel<<<gn, 256, 0, s>>>(w, H, W, nf, ws.rel);
-        init_kernel<<<gn, 256, 0, s>>>(n, ws.po);
+        {   // phase 1: tile-local Borůvka, then the list of the remaining roots
+            const unsigned tiles = (unsigned)(((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile) * nf);
+            tile_boruvka<<<tiles, kTile * kTile, 0, s>>>(w, ws.rel, H, W, nf, ws.po);
+        }
         unsigned* cnt = reinterpret_cast<unsigned*>(ws.flags + 4);
         unsigned* cnt2 = reinterpret_cast<unsigned*>(ws.flags + 5);
-        init_list<<<gn, 256, 0, s>>>(n, ws.list, cnt);
+        init_list<<<gn, 256, 0, s>>>(n, ws.list2, cnt2);
+        if (cudaMemsetAsync(cnt, 0, sizeof(unsigned), s) != cudaSuccess) return BOS_ERR_CUDA;
+        compact_roots<<<gn, 256, 0, s>>>(ws.list2, cnt2, ws.po, ws.list, cnt);
+        unsigned* ecount = reinterpret_cast<unsigned*>(ws.flags + 6);
+        unsigned* E = ws.edges;
+        unsigned* E2 = ws.edges2;
+        unsigned n_edges = (unsigned)(2 * n);                      // round 0: every id, implicitly
+        bool implicit = true;
         for (int round = 0; round < 64; ++round) {                    // Borůvka: ≤ log2(n) rounds
             reset_best_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.best_rel, ws.best_id);
-            edge_max<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel);
-            edge_argmin<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel, ws.best_id);
+            if (implicit) {
+                edge_max<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel);
+                edge_argmin<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel, ws.best_id);
+            } else {
+                const unsigned gl = (unsigned)std::min<size_t>(((size_t)n_edges + 255) / 256, 148 * 16);
+                edge_max_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel);
+                edge_argmin_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel, ws.best_id);
+            }
             if (cudaMemsetAsync(ws.flags, 0, 2 * sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
             hook_list<<<gn, 256, 0, s>>>(H, W, w, ws.list, cnt, ws.po, ws.best_id, ws.best_rel, ws.flags);
             apply_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.best_rel, ws.po);
@@ -388,6 +633,23 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
             compact_roots<<<gn, 256, 0, s>>>(ws.list, cnt, ws.po, ws.list2, cnt2);
             std::swap(ws.list, ws.list2);
             std::swap(cnt, cnt2);
+            // keep only the edges that still cross components (every node now points at its root)
+            const unsigned nb = (unsigned)(((size_t)n_edges + kFiltPerBlock - 1) / kFiltPerBlock);
+            if (implicit) {
+                filter_count<true><<<nb, kFiltThreads, 0, s>>>(E, n_edges, H, W, ws.po, ws.ebits, ws.bcount);
+                scan_counts<<<1, kFiltThreads, 0, s>>>(ws.bcount, nb, ws.boff, ecount);
+                filter_scatter<true><<<nb, kFiltThreads, 0, s>>>(E, n_edges, ws.ebits, ws.boff, E2);
+            } else {
+                filter_count<false><<<nb, kFiltThreads, 0, s>>>(E, n_edges, H, W, ws.po, ws.ebits, ws.bcount);
+                scan_counts<<<1, kFiltThreads, 0, s>>>(ws.bcount, nb, ws.boff, ecount);
+                filter_scatter<false><<<nb, kFiltThreads, 0, s>>>(E, n_edges, ws.ebits, ws.boff, E2);
+            }
+            if (cudaMemcpyAsync(&n_edges, ecount, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return BOS_ERR_CUDA;
+            std::swap(E, E2);
+            implicit = false;
+            if (n_edges == 0) break;                                    // no crossing edge left
         }
         if (cudaMemsetAsync(ws.amax, 0, nf * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(ws.aidx, 0xff, nf * sizeof(unsigned), s) != cudaSuccess)

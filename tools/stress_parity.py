@@ -69,7 +69,7 @@ def main():
     ap.add_argument("--min-m", type=int, default=3)
     ap.add_argument("--max-m", type=int, default=32)
     args = ap.parse_args()
-    bad, worst, t0, c = [], 0.0, time.time(), -1
+    bad, worst, t0, c, worst_case = [], 0.0, time.time(), -1, None
     for k in draw_cases(args.seed, args.cases, args.min_m, args.max_m):
         if time.time() - t0 > args.budget_s:
             break
@@ -78,10 +78,13 @@ def main():
         if args.variant.startswith("ss") and k["M"] <= args.subarray:
             continue
         mx, rms, nan, exc = run_case(k)
-        worst = max(worst, mx)
+        if mx > worst:
+            worst, worst_case = mx, dict(M=k["M"], snr=k["snr"], H=k["H"], W=k["W"], workload=k["workload"])
         if nan or mx > 1e-2 or rms > 1e-3:
             bad.append(dict(k, max=mx, rms=rms, nan=nan, excluded=exc))
-    print(f"cases run: {c + 1}, failures: {len(bad)}, worst max error {worst:.2e} rad")
+    print(f"cases run: {c + 1}, failures: {len(bad)}, worst max error {worst:.2e} rad"
+          f" (kernel choice BOS_THREAD_KERNEL={os.environ.get('BOS_THREAD_KERNEL', 'auto')})")
+    print(f"worst case: {worst_case}")
     for b in bad:
         print(b)
 
