@@ -273,10 +273,11 @@ def measured_fp32_peak(dev_index: int):
 
 
 class StackTimer:
-    """One step = the hot path over a resident stack: raw α of the reference (local frame 0),
-    then every local frame against it (sharding.sharded_stack_step; 2 launches).  Device
-    times with CUDA events on the launching stream, barrier + synchronize around the region,
-    max over ranks."""
+    """One step = the hot path over a resident stack: raw α (and flags) of the reference (local
+    frame 0), then the T−1 flow frames against it (sharding.sharded_stack_step; 2 launches —
+    the reference is demodulated once, as bos_rootmusic_demod_stack does).  Device times with
+    CUDA events on the launching stream, barrier + synchronize around the region, max over
+    ranks."""
 
     def __init__(self, frames, M, ref_mode, dev):
         from paper_1910_11872_b200 import bosrm
@@ -289,16 +290,19 @@ class StackTimer:
 
     def _raw(self, frame):
         H, W = frame.shape
-        self.bosrm.bos_rootmusic_demod(frame.unsqueeze(0), self.M, out_phase=self.ref.view(1, H, W))
+        self.bosrm.bos_rootmusic_demod(frame.unsqueeze(0), self.M, out_phase=self.ref.view(1, H, W),
+                                       flags=self.flags[:1])
         return self.ref
 
     def step(self, ev=None):
         from paper_1910_11872_b200 import sharding
 
         def demod_all(fr, r):
+            # the flow frames (local 1…T−1) against φ_ref; the reference frame itself was
+            # demodulated once by _raw (its own difference output ≡ 0 is not rewritten)
             if ev is not None:
                 ev[0].record(self.stream)
-            self.bosrm.bos_rootmusic_demod(fr, self.M, ref_phase=r, out_phase=self.out, flags=self.flags)
+            self.bosrm.bos_rootmusic_demod(fr[1:], self.M, ref_phase=r, out_phase=self.out[1:], flags=self.flags[1:])
             if ev is not None:
                 ev[1].record(self.stream)
 
@@ -373,7 +377,7 @@ def extra_points(args, dev):
     k = iteration_means(st[1:5], 15)
     f = path_flops(15, *k, 100, 1024, 1024)
     res["c3_m15"] = {"mpix_s": 100 * 1024 * 1024 * 3 / (ms / 1e3) / 1e6, "kernel": kernel_name(15),
-                     "frac_own_model": f * 100 * 1024 * 1024 / (kms / 1e3) / 1e12 / nominal_peak(),
+                     "frac_own_model": f * 99 * 1024 * 1024 / (kms / 1e3) / 1e12 / nominal_peak(),
                      "iters": {"power": k[0], "aberth_y": k[1], "aberth_x": k[2]}}
     del tm, st
     torch.cuda.empty_cache()
@@ -439,8 +443,8 @@ def run_cuda(args, world, rank, local):
     ms_per_step = elapsed_ms / args.steps
 
     # roofline of the dominant kernel (the T-frame demod launch; the ref launch is 1/T of it)
-    f_px = path_flops(M, k_pi, k_aby, k_abx, T, H, W)
-    achieved = f_px * T * plane / (kern_ms / 1e3) / 1e12
+    f_px = path_flops(M, k_pi, k_aby, k_abx, T - 1, H, W)
+    achieved = f_px * (T - 1) * plane / (kern_ms / 1e3) / 1e12     # the timed launch: the T−1 flow frames
     sm_max = float(peaks().get("sm_max_mhz", 1965.0))
     peak = nominal_peak(sm_max)
     traffic = None
@@ -448,7 +452,7 @@ def run_cuda(args, world, rank, local):
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
         if int(tr.get("window_len", -1)) == M:
-            traffic = tr["dram_bytes_per_pixel"] * T * plane   # bytes per stack launch (ncu capture)
+            traffic = tr["dram_bytes_per_pixel"] * (T - 1) * plane   # bytes per flow-frame launch (ncu capture)
     except (OSError, ValueError, KeyError):
         traffic = None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -457,7 +461,7 @@ def run_cuda(args, world, rank, local):
                 "flops_per_px": f_px, "iters": {"power": k_pi, "aberth_y": k_aby, "aberth_x": k_abx},
                 "peak_basis": f"nominal FP32 FMA (the contract): {B200_SMS} SM x {FP32_LANES_PER_SM} lanes x 2 x "
                               f"{sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                "hbm_gbs": (T * plane * 13 + plane * 8) / (kern_ms / 1e3) / 1e9}
+                "hbm_gbs": ((T - 1) * plane * 13 + plane * 4) / (kern_ms / 1e3) / 1e9}
     if mb and mb.get("ffma_tflops"):
         roofline["peak_measured_ffma"] = mb["ffma_tflops"]
         roofline["frac_vs_measured_ffma"] = achieved / mb["ffma_tflops"]

@@ -105,11 +105,15 @@ int bos_rootmusic_demod(const bos_cf32* frames, int n_frames, int H, int W,
 /*
  * bos_rootmusic_demod_stack — a time-lapse stack against its own reference frame
  * (BASELINE north_star: "each flow frame's phase is differenced against the reference
- * frame").  Two stream-ordered launches:
- *   ref_phase_out ← raw α of frames[ref_index];  out[t] ← wrap(α_t − ref_phase_out).
+ * frame").  Stream-ordered launches:
+ *   ref_phase_out ← raw α of frames[ref_index] (and flags[ref_index]);
+ *   out[t] ← wrap(α_t − ref_phase_out) for every t ≠ ref_index (one launch per side of it);
+ *   out[ref_index] ← ref_phase_out − ref_phase_out: exactly 0, NaN where α_ref is — what
+ *   demodulating the reference frame against itself would give, without doing it twice.
  *   ref_index      0 ≤ ref_index < n_frames.
- *   ref_phase_out  DEVICE [H][W] float32, written (caller-owned scratch / result).
- * Other arguments as bos_rootmusic_demod.  out[ref_index] is exactly 0 where finite.
+ *   ref_phase_out  DEVICE [H][W] float32, written (caller-owned scratch / result); must not
+ *                  overlap frames or out_phase.
+ * Other arguments as bos_rootmusic_demod.
  */
 int bos_rootmusic_demod_stack(const bos_cf32* frames, int n_frames, int H, int W,
                               int window_len, int model_order, int ref_index,

@@ -207,6 +207,13 @@ struct Pipe {
 Pipe g_pipe[kPipeDevices];
 std::mutex g_pipe_mutex[kPipeDevices];
 
+// out = wrap(a − a): exactly what the demod's fused difference writes for the reference frame
+// itself (0, or NaN where a is NaN)
+__global__ void self_difference_kernel(const float* __restrict__ a, size_t n, float* __restrict__ out) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = a[i] - a[i];
+}
+
 // Eq.(17): ∂n/∂x = (1/(2 μ f_x)) (n0/L²) φ — a pointwise scale (vectorised, HBM-bound).
 __global__ void index_gradient_kernel(const float* __restrict__ phase, size_t n, float k, float* __restrict__ out) {
     const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -331,11 +338,32 @@ int bos_rootmusic_demod_stack(const bos_cf32* frames, int n_frames, int H, int W
     if (overlaps(ref_phase_out, plane * sizeof(float), frames, plane * (size_t)n_frames * sizeof(bos_cf32)))
         return BOS_ERR_INVALID_ARG;
     if (!is_device_ptr(ref_phase_out)) return BOS_ERR_INVALID_ARG;
+    if (out_phase == nullptr || !is_device_ptr(out_phase)) return BOS_ERR_INVALID_ARG;
+    if (overlaps(ref_phase_out, plane * sizeof(float), out_phase, plane * (size_t)n_frames * sizeof(float)))
+        return BOS_ERR_INVALID_ARG;
+    // the reference frame once (raw α, and its flags); its own output wrap(α_ref − α_ref) is
+    // exactly 0 (NaN where α_ref is) — written by a pointwise kernel instead of demodulating
+    // the frame a second time; the other frames in ≤ 2 launches around it
+    uint8_t* ref_flags = flags != nullptr ? flags + (size_t)ref_index * plane : nullptr;
     rc = demod_impl(frames + (size_t)ref_index * plane, 1, H, W, window_len, model_order, nullptr, ref_phase_out,
-                    nullptr, nullptr, stream, true);
+                    ref_flags, nullptr, stream, true);
     if (rc != BOS_OK) return rc;
-    return demod_impl(frames, n_frames, H, W, window_len, model_order, ref_phase_out, out_phase, flags, nullptr,
-                      stream, true);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned blocks = (unsigned)std::min<size_t>((plane + 255) / 256, 148 * 8);
+    self_difference_kernel<<<blocks, 256, 0, s>>>(ref_phase_out, plane, out_phase + (size_t)ref_index * plane);
+    if (cudaGetLastError() != cudaSuccess) return BOS_ERR_CUDA;
+    if (ref_index > 0) {
+        rc = demod_impl(frames, ref_index, H, W, window_len, model_order, ref_phase_out, out_phase, flags, nullptr,
+                        stream, true);
+        if (rc != BOS_OK) return rc;
+    }
+    const int after = n_frames - ref_index - 1;
+    if (after > 0) {
+        const size_t o = (size_t)(ref_index + 1) * plane;
+        rc = demod_impl(frames + o, after, H, W, window_len, model_order, ref_phase_out, out_phase + o,
+                        flags != nullptr ? flags + o : nullptr, nullptr, stream, true);
+    }
+    return rc;
 }
 
 size_t bos_rootmusic_host_workspace_bytes(int H, int W, int chunk_frames, int with_flags) {
