@@ -119,7 +119,7 @@ def strip_rows_for(M: int, T: int = 100, H: int = 1024, W: int = 1024, sms: int 
     """S the library's launcher picks for window M on a T×H×W launch (launch_strip: halve from
     BOS_STRIP_ROWS while fewer than 4 work items per resident warp, down to 2); None when the
     launch is too small for S ≥ BOS_STRIP_MIN_ROWS and runs the row / warp kernel."""
-    warps_per_sm = (16 if M <= 8 else (12 if M <= 11 else 8)) if strip_kind(M) == 1 else (12 if M <= 18 else 8)
+    warps_per_sm = (16 if M <= 8 else (12 if M <= 11 else 8)) if strip_kind(M) == 1 else (16 if M <= 11 else (12 if M <= 18 else 8))
     row_items = T * H * ((W + 31) // 32)
     S = STRIP_ROWS
     while S > 2 and row_items // S < 4 * warps_per_sm * sms:

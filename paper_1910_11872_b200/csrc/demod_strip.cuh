@@ -375,8 +375,13 @@ __device__ __forceinline__ float im_gamma_h(const float2* win, const cx2 (&u)[M]
 #ifndef BOS_STRIP_IM_WARPS_MAX_M12
 #define BOS_STRIP_IM_WARPS_MAX_M12 18   // measured: M = 15, 16 +6 %, 17 +3 %, 18 +2 %; M = 20 −4 % (shared memory caps it at 11 warps)
 #endif
+#ifndef BOS_STRIP_IM_WARPS_MAX_M16
+#define BOS_STRIP_IM_WARPS_MAX_M16 11   // largest M given 16 warps/SM (128 registers): M = 11 +5 %; 14…16 spill there and lose 2…13 %
+#endif
 template <int M>
-constexpr int strip_im_min_blocks() { return M <= BOS_STRIP_IM_WARPS_MAX_M12 ? 12 : 8; }
+constexpr int strip_im_min_blocks() {
+    return M <= BOS_STRIP_IM_WARPS_MAX_M16 ? 16 : (M <= BOS_STRIP_IM_WARPS_MAX_M12 ? 12 : 8);
+}
 
 template <int M, bool COUNT>
 __global__ void __launch_bounds__(32, strip_im_min_blocks<M>())
