@@ -96,3 +96,25 @@ def test_strip_im_kernel_parity(M, monkeypatch):
         o, ofl = R.demod_frame(f.numpy(), M)
         assert_parity(g, o, ofl, f"strip_rs M={M} {snr} dB", gpu_flags=gfl)
         assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"strip_rs M={M} {snr} dB")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M", [3, 8, 11, 13, 16, 24, 32])
+def test_strip_kernels_minimum_and_thin_frames(M, monkeypatch):
+    """Edge shapes on the forced strip kernels: the smallest legal frame (H = W = M), a frame
+    one column wide of a 32-column block past a block boundary (W = 33), a single strip row
+    (H = M) against many rows, several frames in one launch — parity with the oracle on every
+    pixel (all windows clamped), and the kind-1 kernel still bitwise the row kernel."""
+    for H, W, T in ((M, M, 2), (M + 5, 33, 3), (M, 70, 2)):
+        w = synth.workload("C3", H=H, W=W, seed=17)
+        fr = torch.stack([synth.make_frame(w, t + 1, snr_db=15.0) for t in range(T)])
+        monkeypatch.setenv("BOS_THREAD_KERNEL", "strip")
+        g, gfl, wx, wy = (x.cpu().numpy() for x in bosrm.bos_rootmusic_demod_ex(fr.to(DEV), M, flags=True))
+        for t in range(T):
+            o, ofl = R.demod_frame(fr[t].numpy(), M)
+            assert_parity(g[t], o, ofl, f"strip M={M} {H}x{W} t={t}", gpu_flags=gfl[t], max_interior_excluded_frac=1.0)
+            assert_excluded_valid(fr[t].numpy(), M, g[t], wx[t], wy[t], ofl, f"strip M={M} {H}x{W} t={t}")
+        if M <= 10 or M in (12, 13):
+            b = _run(fr.to(DEV), M, monkeypatch, row=True)
+            a = _run(fr.to(DEV), M, monkeypatch, row=False)
+            _assert_same(a, b, f"M={M} {H}x{W}")
