@@ -12,9 +12,11 @@
 // chosen neighbour's root with the offset that satisfies the edge, and pointer jumping sums
 // offsets to the root.  The reliabilities are computed in FP64 with the oracle's operation
 // order and IEEE round-to-nearest intrinsics, so the edge order — and hence every 2π multiple —
-// is identical to the FP64 oracle (oracle/unwrap.py).  After every round the edges that still
-// cross components are compacted (order-preserving) into a list, so later rounds touch only
-// those: round 0 scans all 2·H·W edges, later rounds a shrinking fraction.
+// is identical to the FP64 oracle (oracle/unwrap.py).  Phase 1 (tile_boruvka) contracts
+// inside 16×16 tiles in shared memory and lists the remaining roots and crossing edges; the
+// global rounds then touch only those lists: after every round the still-crossing edges are
+// compacted (order-preserving), and only the tile phase's roots are re-linked (every node
+// reaches its current root in two hops, find2); one full re-link at the end.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -62,11 +64,17 @@ __device__ __forceinline__ unsigned long long pk(int parent, int off) {
 }
 __device__ __forceinline__ int par(unsigned long long w) { return (int)(unsigned)(w & 0xffffffffull); }
 __device__ __forceinline__ int ofs(unsigned long long w) { return (int)(unsigned)(w >> 32); }
-
-__global__ void init_kernel(size_t n, unsigned long long* po) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        po[i] = pk((int)i, 0);
+// (current root, 2π offset to it) of node p.  Invariant of the global rounds: every node points
+// at a "former root" (a root when the tile phase ended) or at a current root, and every former
+// root's entry is kept pointing at its current root (relink_list) — so two hops reach the root.
+__device__ __forceinline__ unsigned long long find2(const unsigned long long* po, int p) {
+    const unsigned long long w = po[p];
+    const int r = par(w);
+    if (r == p) return w;
+    const unsigned long long w2 = po[r];
+    return pk(par(w2), ofs(w) + ofs(w2));
 }
+
 
 // edge id e = 2p (p → p+1) or 2p+1 (p → p+W), p = frame·H·W + y·W + x (a batch of frames is one
 // forest of independent grids); returns false for the missing border edges
@@ -89,7 +97,7 @@ __device__ __forceinline__ void edge_max_one(unsigned e, int H, int W, const dou
                                              const unsigned long long* __restrict__ po, unsigned long long* best_rel) {
     int p, q;
     if (!edge_ends(e, H, W, p, q)) return;
-    const int rp = par(po[p]), rq = par(po[q]);
+    const int rp = par(find2(po, p)), rq = par(find2(po, q));
     if (rp == rq) return;
     const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
     atomicMax(best_rel + rp, key);
@@ -101,27 +109,13 @@ __device__ __forceinline__ void edge_argmin_one(unsigned e, int H, int W, const 
                                                 const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
     int p, q;
     if (!edge_ends(e, H, W, p, q)) return;
-    const int rp = par(po[p]), rq = par(po[q]);
+    const int rp = par(find2(po, p)), rq = par(find2(po, q));
     if (rp == rq) return;
     const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
     if (key == best_rel[rp]) atomicMin(best_id + rp, e);
     if (key == best_rel[rq]) atomicMin(best_id + rq, e);
 }
-// round 0: every edge id 0 … 2·H·W·F − 1 (border ids drop out in edge_ends)
-__global__ void edge_max(int H, int W, int F, const double* __restrict__ rel,
-                         const unsigned long long* __restrict__ po, unsigned long long* best_rel) {
-    const size_t ne = 2 * (size_t)H * W * F;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x)
-        edge_max_one((unsigned)e, H, W, rel, po, best_rel);
-}
-__global__ void edge_argmin(int H, int W, int F, const double* __restrict__ rel,
-                            const unsigned long long* __restrict__ po,
-                            const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
-    const size_t ne = 2 * (size_t)H * W * F;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (size_t)gridDim.x * blockDim.x)
-        edge_argmin_one((unsigned)e, H, W, rel, po, best_rel, best_id);
-}
-// later rounds: only the edges that still cross components (the compacted list)
+// the global rounds: only the edges that still cross components (the compacted list)
 __global__ void edge_max_list(const unsigned* __restrict__ list, unsigned n, int H, int W,
                               const double* __restrict__ rel, const unsigned long long* __restrict__ po,
                               unsigned long long* best_rel) {
@@ -143,7 +137,6 @@ constexpr int kFiltThreads = 256;
 constexpr int kFiltPerThread = 8;                              // one flag byte per thread
 constexpr int kFiltPerBlock = kFiltThreads * kFiltPerThread;
 
-template <bool IMPLICIT>
 __device__ __forceinline__ unsigned crossing_bits(const unsigned* __restrict__ list, unsigned n_in, int H, int W,
                                                   const unsigned long long* __restrict__ po, unsigned base) {
     unsigned m = 0;
@@ -151,9 +144,9 @@ __device__ __forceinline__ unsigned crossing_bits(const unsigned* __restrict__ l
     for (int j = 0; j < kFiltPerThread; ++j) {
         const unsigned idx = base + j;
         if (idx >= n_in) break;
-        const unsigned e = IMPLICIT ? idx : list[idx];
+        const unsigned e = list[idx];
         int p, q;
-        if (edge_ends(e, H, W, p, q) && par(po[p]) != par(po[q])) m |= 1u << j;
+        if (edge_ends(e, H, W, p, q) && par(find2(po, p)) != par(find2(po, q))) m |= 1u << j;
     }
     return m;
 }
@@ -182,12 +175,11 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total)
     if (total != nullptr) *total = wsum[kFiltThreads / 32 - 1];
     return before;
 }
-template <bool IMPLICIT>
 __global__ void __launch_bounds__(kFiltThreads) filter_count(const unsigned* __restrict__ list, unsigned n_in, int H,
                                                               int W, const unsigned long long* __restrict__ po,
                                                               uint8_t* __restrict__ bits, unsigned* __restrict__ bcount) {
     const unsigned t = blockIdx.x * kFiltThreads + threadIdx.x;
-    const unsigned m = crossing_bits<IMPLICIT>(list, n_in, H, W, po, t * kFiltPerThread);
+    const unsigned m = crossing_bits(list, n_in, H, W, po, t * kFiltPerThread);
     bits[t] = (uint8_t)m;
     unsigned tot;
     block_excl_scan((unsigned)__popc(m), &tot);
@@ -208,7 +200,6 @@ __global__ void __launch_bounds__(kFiltThreads) scan_counts(const unsigned* __re
     }
     if (threadIdx.x == 0) *count = tot;
 }
-template <bool IMPLICIT>
 __global__ void __launch_bounds__(kFiltThreads) filter_scatter(const unsigned* __restrict__ list, unsigned n_in,
                                                                 const uint8_t* __restrict__ bits,
                                                                 const unsigned* __restrict__ boff,
@@ -219,7 +210,7 @@ __global__ void __launch_bounds__(kFiltThreads) filter_scatter(const unsigned* _
     const unsigned base = t * kFiltPerThread;
 #pragma unroll
     for (int j = 0; j < kFiltPerThread; ++j)
-        if ((m >> j) & 1u) out[pos++] = IMPLICIT ? base + j : list[base + j];
+        if ((m >> j) & 1u) out[pos++] = list[base + j];
 }
 
 // e(a→b) = (γ(w_b − w_a) − (w_b − w_a)) / 2π  ∈ {−1, 0, 1}: required k(b) − k(a)
@@ -246,7 +237,10 @@ __device__ __forceinline__ int tpar(unsigned v) { return (int)(v & 0xffffu); }
 __device__ __forceinline__ int tofs(unsigned v) { return (int)v >> 16; }
 
 __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_boruvka(const float* __restrict__ w, const double* __restrict__ rel,
-                                                              int H, int W, int F, unsigned long long* __restrict__ po) {
+                                                              int H, int W, int F, unsigned long long* __restrict__ po,
+                                                              unsigned* __restrict__ roots, unsigned* __restrict__ roots0,
+                                                              unsigned* __restrict__ nroots, unsigned* __restrict__ edges,
+                                                              unsigned* __restrict__ nedges) {
     __shared__ unsigned node[kTile * kTile];                 // (local parent, 2π offset to it)
     __shared__ unsigned long long bkey[kTile * kTile];       // best incident key per component root
     __shared__ unsigned bid[kTile * kTile];                  // best incident edge id per component root
@@ -326,8 +320,31 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
             if (!__syncthreads_or(ch)) break;
         }
     }
+    // outputs: the node entries, the list of the remaining roots (twice: the global rounds'
+    // working list and the former-root list of find2), and the edges that still cross
+    // components (this node's right and down edges), appended block by block
+    __shared__ unsigned cnt_r, cnt_e, base_r, base_e;
+    if (l == 0) cnt_r = cnt_e = 0u;
+    __syncthreads();
+    const unsigned v = node[l];
+    const bool is_root = valid && tpar(v) == l;
+    const bool cr = ((has & 1u) != 0) && (ol[0] < 0 || tpar(node[ol[0]]) != tpar(v));
+    const bool cd = ((has & 2u) != 0) && (ol[1] < 0 || tpar(node[ol[1]]) != tpar(v));
+    const unsigned my_r = is_root ? atomicAdd(&cnt_r, 1u) : 0u;
+    const unsigned my_e = (cr || cd) ? atomicAdd(&cnt_e, (unsigned)cr + (unsigned)cd) : 0u;
+    __syncthreads();
+    if (l == 0) {
+        base_r = atomicAdd(nroots, cnt_r);
+        base_e = atomicAdd(nedges, cnt_e);
+    }
+    __syncthreads();
+    if (is_root) {
+        roots[base_r + my_r] = (unsigned)p;
+        roots0[base_r + my_r] = (unsigned)p;
+    }
+    if (cr) edges[base_e + my_e] = eid[0];
+    if (cd) edges[base_e + my_e + (cr ? 1u : 0u)] = eid[1];
     if (valid) {
-        const unsigned v = node[l];
         const int rl = tpar(v);
         const int gr = (int)((size_t)f * plane + (size_t)(y0 + rl / kTile) * W + (x0 + rl % kTile));
         po[p] = pk(gr, tofs(v));
@@ -337,11 +354,6 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
 // ---- root lists: after the first rounds most nodes are not roots, so the per-round work that
 // only concerns roots (reset, hook, compression of the root chains) runs over a compact list
 // of the current roots; one full pass then re-links every node to its new root.
-__global__ void init_list(size_t n, unsigned* list, unsigned* count) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        list[i] = (unsigned)i;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned)n;
-}
 __global__ void reset_best_list(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
                                 unsigned long long* best_rel, unsigned* best_id) {
     const unsigned n = *count;
@@ -364,7 +376,7 @@ __global__ void hook_list(int H, int W, const float* __restrict__ w, const unsig
             const unsigned e = best_id[c];
             int p, q;
             edge_ends(e, H, W, p, q);
-            const unsigned long long wp = po[p], wq = po[q];
+            const unsigned long long wp = find2(po, p), wq = find2(po, q);
             const bool pin = par(wp) == c;
             const int pc = pin ? p : q, oth = pin ? q : p;
             const unsigned long long wc = pin ? wp : wq, wo = pin ? wq : wp;
@@ -405,6 +417,18 @@ __global__ void jump_list(const unsigned* __restrict__ list, const unsigned* __r
 // their final roots (after jump_list), and only roots' entries are read, so one pass suffices
 __global__ void relink_all(size_t n, unsigned long long* po) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long wi = po[i];
+        const int p = par(wi);
+        const unsigned long long wp = po[p];
+        const int pp = par(wp);
+        if (pp != p) po[i] = pk(pp, ofs(wi) + ofs(wp));
+    }
+}
+// the former roots (the tile phase's roots, `list0`) re-pointed at their current roots after a
+// round's hooks and jumps — the only entries the two-hop lookup (find2) reads through
+__global__ void relink_list(const unsigned* __restrict__ list, unsigned n, unsigned long long* po) {
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned i = list[k];
         const unsigned long long wi = po[i];
         const int p = par(wi);
         const unsigned long long wp = po[p];
@@ -491,6 +515,7 @@ struct Ws {
     double* rel;
     unsigned long long* po;           // packed (parent, 2π offset) nodes
     unsigned *list, *list2;           // current roots / next round's roots
+    unsigned* list0;                  // former roots (the tile phase's), relinked every round
     unsigned long long* best_rel;
     unsigned* best_id;
     int* flags;                  // [0] hooked, [1] changed, [2] scratch, [4] / [5] list counts, [6] edge count
@@ -512,6 +537,7 @@ size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
     char* p1 = take(n * sizeof(unsigned long long));
     char* l1 = take(n * sizeof(unsigned));
     char* l2 = take(n * sizeof(unsigned));
+    char* l0 = take(n * sizeof(unsigned));
     char* br = take(n * sizeof(unsigned long long));
     char* bi = take(n * sizeof(unsigned));
     char* fl = take(8 * sizeof(int));
@@ -528,6 +554,7 @@ size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
         ws->po = (unsigned long long*)p1;
         ws->list = (unsigned*)l1;
         ws->list2 = (unsigned*)l2;
+        ws->list0 = (unsigned*)l0;
         ws->best_rel = (unsigned long long*)br;
         ws->best_id = (unsigned*)bi;
         ws->flags = (int*)fl;
@@ -585,30 +612,30 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
         Ws ws;
         ws_layout(n, nf, static_cast<char*>(d_workspace), &ws);
         const unsigned gn = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
-        const unsigned ge = (unsigned)std::min<size_t>((2 * n + 255) / 256, 148 * 16);
         const float* w = wrapped + (size_t)f0 * plane;
         float* out = unwrapped + (size_t)f0 * plane;
         reliability_kernel<<<gn, 256, 0, s>>>(w, H, W, nf, ws.rel);
-        {   // phase 1: tile-local Borůvka, then the list of the remaining roots
-            const unsigned tiles = (unsigned)(((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile) * nf);
-            tile_boruvka<<<tiles, kTile * kTile, 0, s>>>(w, ws.rel, H, W, nf, ws.po);
-        }
         unsigned* cnt = reinterpret_cast<unsigned*>(ws.flags + 4);
         unsigned* cnt2 = reinterpret_cast<unsigned*>(ws.flags + 5);
-        init_list<<<gn, 256, 0, s>>>(n, ws.list2, cnt2);
-        if (cudaMemsetAsync(cnt, 0, sizeof(unsigned), s) != cudaSuccess) return BOS_ERR_CUDA;
-        compact_roots<<<gn, 256, 0, s>>>(ws.list2, cnt2, ws.po, ws.list, cnt);
         unsigned* ecount = reinterpret_cast<unsigned*>(ws.flags + 6);
         unsigned* E = ws.edges;
         unsigned* E2 = ws.edges2;
-        unsigned n_edges = (unsigned)(2 * n);                      // round 0: every id, implicitly
-        bool implicit = true;
+        // phase 1: tile-local Borůvka; it also emits the remaining roots and crossing edges
+        if (cudaMemsetAsync(ws.flags + 4, 0, 3 * sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
+        {
+            const unsigned tiles = (unsigned)(((W + kTile - 1) / kTile) * ((H + kTile - 1) / kTile) * nf);
+            tile_boruvka<<<tiles, kTile * kTile, 0, s>>>(w, ws.rel, H, W, nf, ws.po, ws.list, ws.list0, cnt, E, ecount);
+        }
+        unsigned host_counts[3];
+        if (cudaMemcpyAsync(host_counts, ws.flags + 4, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return BOS_ERR_CUDA;
+        const unsigned n_former = host_counts[0];
+        unsigned n_edges = host_counts[2];
         for (int round = 0; round < 64; ++round) {                    // Borůvka: ≤ log2(n) rounds
             reset_best_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.best_rel, ws.best_id);
-            if (implicit) {
-                edge_max<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel);
-                edge_argmin<<<ge, 256, 0, s>>>(H, W, nf, ws.rel, ws.po, ws.best_rel, ws.best_id);
-            } else {
+            if (n_edges == 0) break;                                    // no crossing edge: done
+            {
                 const unsigned gl = (unsigned)std::min<size_t>(((size_t)n_edges + 255) / 256, 148 * 16);
                 edge_max_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel);
                 edge_argmin_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel, ws.best_id);
@@ -628,29 +655,25 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
                 if (!host_flags[1]) break;
             }
             if (!host_flags[0]) break;                                  // nothing hooked: one tree per frame
-            relink_all<<<gn, 256, 0, s>>>(n, ws.po);
+            {
+                const unsigned gf = (unsigned)std::min<size_t>(((size_t)n_former + 255) / 256, 148 * 16);
+                if (n_former > 0) relink_list<<<gf, 256, 0, s>>>(ws.list0, n_former, ws.po);
+            }
             if (cudaMemsetAsync(cnt2, 0, sizeof(unsigned), s) != cudaSuccess) return BOS_ERR_CUDA;
             compact_roots<<<gn, 256, 0, s>>>(ws.list, cnt, ws.po, ws.list2, cnt2);
             std::swap(ws.list, ws.list2);
             std::swap(cnt, cnt2);
             // keep only the edges that still cross components (every node now points at its root)
             const unsigned nb = (unsigned)(((size_t)n_edges + kFiltPerBlock - 1) / kFiltPerBlock);
-            if (implicit) {
-                filter_count<true><<<nb, kFiltThreads, 0, s>>>(E, n_edges, H, W, ws.po, ws.ebits, ws.bcount);
-                scan_counts<<<1, kFiltThreads, 0, s>>>(ws.bcount, nb, ws.boff, ecount);
-                filter_scatter<true><<<nb, kFiltThreads, 0, s>>>(E, n_edges, ws.ebits, ws.boff, E2);
-            } else {
-                filter_count<false><<<nb, kFiltThreads, 0, s>>>(E, n_edges, H, W, ws.po, ws.ebits, ws.bcount);
-                scan_counts<<<1, kFiltThreads, 0, s>>>(ws.bcount, nb, ws.boff, ecount);
-                filter_scatter<false><<<nb, kFiltThreads, 0, s>>>(E, n_edges, ws.ebits, ws.boff, E2);
-            }
+            filter_count<<<nb, kFiltThreads, 0, s>>>(E, n_edges, H, W, ws.po, ws.ebits, ws.bcount);
+            scan_counts<<<1, kFiltThreads, 0, s>>>(ws.bcount, nb, ws.boff, ecount);
+            filter_scatter<<<nb, kFiltThreads, 0, s>>>(E, n_edges, ws.ebits, ws.boff, E2);
             if (cudaMemcpyAsync(&n_edges, ecount, sizeof(unsigned), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                 cudaStreamSynchronize(s) != cudaSuccess)
                 return BOS_ERR_CUDA;
             std::swap(E, E2);
-            implicit = false;
-            if (n_edges == 0) break;                                    // no crossing edge left
         }
+        relink_all<<<gn, 256, 0, s>>>(n, ws.po);                        // every node → its final root
         if (cudaMemsetAsync(ws.amax, 0, nf * sizeof(unsigned long long), s) != cudaSuccess ||
             cudaMemsetAsync(ws.aidx, 0xff, nf * sizeof(unsigned), s) != cudaSuccess)
             return BOS_ERR_CUDA;

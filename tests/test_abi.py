@@ -152,10 +152,10 @@ def test_unwrap_workspace_and_errors(L):
     def edges(n):       # two crossing-edge lists (2n ids), filter flag bytes, per-block counts/offsets
         nb = (2 * n + 2047) // 2048
         return 2 * al(4 * 2 * n) + al(nb * 256) + 2 * al(4 * nb)
-    expect = al(8 * n) + 4 * al(4 * n) + al(8 * n) + al(4 * n) + al(16) + al(8) + al(4) + edges(n)
+    expect = al(8 * n) + 5 * al(4 * n) + al(8 * n) + al(4 * n) + al(16) + al(8) + al(4) + edges(n)
     assert L.bos_unwrap_workspace_bytes(100, 64, 1) == expect
     n3 = 3 * n
-    expect3 = al(8 * n3) + 4 * al(4 * n3) + al(8 * n3) + al(4 * n3) + al(16) + al(24) + al(12) + edges(n3)
+    expect3 = al(8 * n3) + 5 * al(4 * n3) + al(8 * n3) + al(4 * n3) + al(16) + al(24) + al(12) + edges(n3)
     assert L.bos_unwrap_workspace_bytes(100, 64, 3) == expect3
     assert L.bos_unwrap_workspace_bytes(0, 5, 1) == 0
     assert L.bos_unwrap(None, 1, 8, 8, None, None, 0, None) == bosrm.BOS_ERR_INVALID_ARG
