@@ -78,11 +78,13 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
                          cudaStream_t s) {
     const dim3 block(kBX, kBY, 1);
     constexpr int kKind = strip_kind<M>();
-    if constexpr (!FB && !COUNT && kKind > 0) {
-        // paper path: the strip kernels (demod_strip.cuh); small launches fall through
+    if constexpr (!FB && kKind > 0) {
+        // paper path: the strip kernels (demod_strip.cuh); small launches fall through.  The
+        // counting variant (COUNT) takes the same route, so the iteration counts of the flop
+        // model are those of the kernel that runs.
         if (thread_kernel_forced() != 1) {
             const cudaError_t e =
-                launch_strip<M, false, kKind>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters, s);
+                launch_strip<M, COUNT, kKind>(frames, n_frames, H, W, ref, out, flags, omega_x, omega_y, counters, s);
             if (e != cudaErrorNotReady) return e;
         }
     }
