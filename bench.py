@@ -76,6 +76,7 @@ def peaks():
 
 STRIP_ROWS = 16      # BOS_STRIP_ROWS: rows per strip work item on large launches (launch_strip)
 STRIP_MIN_ROWS = 8   # BOS_STRIP_MIN_ROWS: launches that would get shorter strips run the row kernel
+STRIP_SMALL_MIN_M = 17   # BOS_STRIP_SMALL_MIN_M: ... except the implicit kernel from this M
 
 
 def strip_kind(M: int) -> int:
@@ -124,7 +125,8 @@ def strip_rows_for(M: int, T: int = 100, H: int = 1024, W: int = 1024, sms: int 
     S = STRIP_ROWS
     while S > 2 and row_items // S < 4 * warps_per_sm * sms:
         S //= 2
-    return S if S >= STRIP_MIN_ROWS else None
+    any_size = strip_kind(M) == 2 and M >= STRIP_SMALL_MIN_M
+    return S if (S >= STRIP_MIN_ROWS or any_size) else None
 
 
 def path_flops(M: int, k_pi: float, k_aby: float, k_abx: float, T: int, H: int, W: int) -> float:

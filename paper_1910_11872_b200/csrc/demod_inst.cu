@@ -63,8 +63,12 @@ cudaError_t launch_strip(const float2* frames, int n_frames, int H, int W, const
     // S rows per item; small launches use shorter strips so every resident warp gets ≥ 4 items
     int S = BOS_STRIP_ROWS;
     while (S > 2 && row_items / S < 4 * resident) S >>= 1;
-    if (S < BOS_STRIP_MIN_ROWS && thread_kernel_forced() != 2)
-        return cudaErrorNotReady;                                   // too small: the caller uses the row kernel
+    // too small for long strips: the row kernel, except where the row / warp kernels are the
+    // weaker choice even then (the implicit kernel from BOS_STRIP_SMALL_MIN_M: a 512² frame at
+    // M = 20 runs 359 vs 255 Mpixel/s; up to M = 15 the row kernel's finer work items win)
+    constexpr bool kAnySize = KIND == 2 && M >= BOS_STRIP_SMALL_MIN_M;
+    if (S < BOS_STRIP_MIN_ROWS && thread_kernel_forced() != 2 && !kAnySize)
+        return cudaErrorNotReady;
     const long long items = (long long)n_frames * ((H + S - 1) / S) * nbx;
     const long long grid = std::min<long long>((items + WARPS - 1) / WARPS, 0x7fffffffLL);
     kern<<<(unsigned)grid, WARPS * 32, smem, s>>>(frames, n_frames, H, W, S, ref, out, flags, omega_x, omega_y,

@@ -64,6 +64,9 @@ constexpr float kPowerErrTol = BOS_POWER_ERR_TOL;
 #ifndef BOS_STRIP_MIN_ROWS
 #define BOS_STRIP_MIN_ROWS 8     // smaller launches run on the row kernel (launch_strip)
 #endif
+#ifndef BOS_STRIP_SMALL_MIN_M
+#define BOS_STRIP_SMALL_MIN_M 17 // from this M the implicit kernel also runs launches too small for 8-row strips
+#endif
 #ifndef BOS_STRIP_WARPS
 #define BOS_STRIP_WARPS 1
 #endif

@@ -44,5 +44,6 @@ def test_strip_kind_and_rows_mirror_the_launcher():
     # one 512² frame is too small for 8-row strips: the row kernel runs it
     assert bench.strip_rows_for(8, 1, 512, 512) is None
     assert bench.kernel_name(8, 1, 512, 512).startswith("bos::demod_kernel<8")
+    assert bench.kernel_name(20, 1, 512, 512) == "bos::demod_strip_im_kernel<20,false>"   # any size from M = 17
     assert bench.kernel_name(8) == "bos::demod_strip_kernel<8,false>"
     assert bench.kernel_name(20) == "bos::demod_strip_im_kernel<20,false>"
