@@ -31,15 +31,17 @@ inline int thread_kernel_forced() {
 // cudaErrorNotReady without launching (a cold start per 2–4 rows costs more than the sliding
 // covariance saves: C2 512² pairs ran 9 % slower) and go to the row kernel.
 // KIND (strip_kind): 1 = R_y slid in registers (demod_strip_kernel), 2 = no R_y, implicit
-// power iteration (demod_strip_im_kernel)
+// power iteration (demod_strip_im_kernel), 3 = the same for the FB variant (demod_strip_imfb_kernel)
 template <int M, bool COUNT, int KIND>
 cudaError_t launch_strip(const float2* frames, int n_frames, int H, int W, const float* ref, float* out,
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
     constexpr int WARPS = KIND == 1 ? strip_warps<M>() : 1;
-    constexpr size_t smem = KIND == 1 ? strip_smem_bytes<M>() : strip_im_smem_bytes<M>();
+    constexpr size_t smem = KIND == 1 ? strip_smem_bytes<M>()
+                          : (KIND == 2 ? strip_im_smem_bytes<M>() : strip_imfb_smem_bytes<M>());
     auto kern = [] {
         if constexpr (KIND == 2) return demod_strip_im_kernel<M, COUNT>;
+        else if constexpr (KIND == 3) return demod_strip_imfb_kernel<M, COUNT>;
         else return demod_strip_kernel<M, COUNT>;
     }();
     int dev = 0;
@@ -66,7 +68,7 @@ cudaError_t launch_strip(const float2* frames, int n_frames, int H, int W, const
     // too small for long strips: the row kernel, except where the row / warp kernels are the
     // weaker choice even then (the implicit kernel from BOS_STRIP_SMALL_MIN_M: a 512² frame at
     // M = 20 runs 359 vs 255 Mpixel/s; up to M = 15 the row kernel's finer work items win)
-    constexpr bool kAnySize = KIND == 2 && M >= BOS_STRIP_SMALL_MIN_M;
+    constexpr bool kAnySize = (KIND == 2 || KIND == 3) && M >= BOS_STRIP_SMALL_MIN_M;
     if (S < BOS_STRIP_MIN_ROWS && thread_kernel_forced() != 2 && !kAnySize)
         return cudaErrorNotReady;
     const long long items = (long long)n_frames * ((H + S - 1) / S) * nbx;
@@ -81,8 +83,8 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
     const dim3 block(kBX, kBY, 1);
-    constexpr int kKind = strip_kind<M>();
-    if constexpr (!FB && kKind > 0) {
+    constexpr int kKind = FB ? (M >= kStripFbMinM ? 3 : 0) : strip_kind<M>();
+    if constexpr (kKind > 0) {
         // paper path: the strip kernels (demod_strip.cuh); small launches fall through.  The
         // counting variant (COUNT) takes the same route, so the iteration counts of the flop
         // model are those of the kernel that runs.

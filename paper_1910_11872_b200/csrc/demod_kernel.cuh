@@ -44,7 +44,15 @@ constexpr int kPowerMaxIt = 64;       // power-iteration cap (NONCONVERGED beyon
 #ifndef BOS_POWER_TOL
 #define BOS_POWER_TOL 1e-8f
 #endif
-constexpr float kPowerTol = BOS_POWER_TOL;    // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2) ≤ 3.3e-4 where σ1²/σ2² ≥ 1.3)
+constexpr float kPowerTol = BOS_POWER_TOL;
+// Clamped border windows [R1] (repeated rows / columns) leave α ill-conditioned: a held-out
+// stress case (M = 17, −5 dB, a frame corner) missed the bar by 0.0012 rad with the 1e-8 stop
+// and matched to 1.2e-4 rad at FP32 noise.  Border windows iterate to it (a few % of a large
+// frame's pixels, in the warps of its edge strips only).
+#ifndef BOS_POWER_TOL_BORDER
+#define BOS_POWER_TOL_BORDER 1e-12f
+#endif
+constexpr float kPowerTolBorder = BOS_POWER_TOL_BORDER;    // ‖u_{k+1} − u_k‖² stop (error ≈ ‖Δu‖·λ2/(λ1−λ2) ≤ 3.3e-4 where σ1²/σ2² ≥ 1.3)
 // Spatial smoothing (demod_ss.cuh): the order-m eigenvector feeds a degree-(2m−2) polynomial
 // whose signal pair is a near-double root, so its angle is far more sensitive to u than at
 // order M; a 3×3…m×m iteration is cheap, so it runs to FP32 noise (stress: 0.01–0.15 rad
@@ -100,6 +108,28 @@ constexpr int kAberthMaxIt = 40;      // Aberth sweep cap
 #define BOS_ABERTH_TOL2 2e-3f
 #endif
 constexpr float kAberthTol2 = BOS_ABERTH_TOL2;  // thread kernel (demod_kernel, demod_ss)
+// Per-window-size loose tolerance of the thread / strip kernels' paper path: held-out stress
+// seeds (tools/stress_r02_regressions.jsonl) found loose-stop misplacements at M = 4 (−5 dB,
+// an approximation pair sharing one root, 1.39 rad) and M = 32 (10 dB, a clamped border window,
+// 0.063 rad) that a tighter stop removes; the windows there are cheap (M ≤ 5: K ≤ 4 roots) or
+// already long (M ≥ 21: the warp kernel used 1e-3 for the same reason).
+#ifndef BOS_ABERTH_TOL2_SMALL_M
+#define BOS_ABERTH_TOL2_SMALL_M 1e-4f
+#endif
+#ifndef BOS_ABERTH_SMALL_MAX_M
+#define BOS_ABERTH_SMALL_MAX_M 5
+#endif
+#ifndef BOS_ABERTH_TOL2_LARGE_M
+#define BOS_ABERTH_TOL2_LARGE_M 1e-3f
+#endif
+#ifndef BOS_ABERTH_LARGE_MIN_M
+#define BOS_ABERTH_LARGE_MIN_M 21
+#endif
+template <int M>
+constexpr float aberth_tol2() {
+    return M <= BOS_ABERTH_SMALL_MAX_M ? BOS_ABERTH_TOL2_SMALL_M
+                                       : (M >= BOS_ABERTH_LARGE_MIN_M ? BOS_ABERTH_TOL2_LARGE_M : kAberthTol2);
+}
 #ifndef BOS_ABERTH_TOL2_WIDE
 #define BOS_ABERTH_TOL2_WIDE 1e-3f
 #endif
@@ -614,7 +644,7 @@ __device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory")
 
 template <int M, int STRIDE = kThreads, bool FENCE = false>
 __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const cx2* Rs, cx2 (&u)[M], bool& ok,
-                                                    float* lam2_out = nullptr) {
+                                                    float* lam2_out = nullptr, float tol = kPowerTol) {
     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Rs[tri_off<M>(i + 1, i) * STRIDE]));
@@ -660,7 +690,7 @@ __device__ __forceinline__ int power_iteration_smem(const float (&Rd)[M], const 
             u[i] = yn;
         }
         ++n;
-        if (diff < kPowerTol) {
+        if (diff < tol) {
             ok = true;
             if (lam2_out != nullptr) *lam2_out = nrm2;     // ‖R u‖² = λ1² at convergence
             break;
@@ -728,7 +758,7 @@ __device__ __forceinline__ float roots_and_phase(const float2* win, const cx2 (&
         int its = 0;
         float marg = CUDART_INF_F;
         float2 zs, z2;
-        float tol2 = ((BOS_WEAK_MODE == 1 || WEAK_TIGHT) && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
+        float tol2 = ((BOS_WEAK_MODE == 1 || WEAK_TIGHT) && (fl & kFlagWeakInternal)) ? fminf(kAberthLowSnrTol2, aberth_tol2<M>()) : aberth_tol2<M>();
 #pragma unroll 1
         for (int attempt = 0;; ++attempt) {
             its += aberth_sym<N, newton_stop<FB, M>()>(c, z, ok, tol2, BOS_WEAK_MODE == 0 && (fl & kFlagWeakInternal));
@@ -846,7 +876,7 @@ __device__ __forceinline__ float roots_and_phase_q(const float2* win, QFn&& qfn,
         // WEAK_TIGHT (large windows): a weak-tone window starts from the tight tolerance, the
         // warp kernel's rule (kLowSnrRatio) — with the Newton-ratio stop alone the loose sweeps
         // misplaced a 0 dB pixel at M = 22 (2.4 rad, tests/test_gpu_strip.py)
-        float tol2 = ((BOS_WEAK_MODE == 1 || WEAK_TIGHT) && (fl & kFlagWeakInternal)) ? kAberthLowSnrTol2 : kAberthTol2;
+        float tol2 = ((BOS_WEAK_MODE == 1 || WEAK_TIGHT) && (fl & kFlagWeakInternal)) ? fminf(kAberthLowSnrTol2, aberth_tol2<M>()) : aberth_tol2<M>();
         // roots_and_phase's attempt loop and runner-up polish as one loop with ONE copy of the
         // polish code (the thread kernels are instruction-cache bound at M ≥ 13: ncu no_inst
         // stalls 23 %):  stage 0: loose sweeps, polish the selected root;  1: tight sweeps
@@ -1109,7 +1139,8 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                 float2 v[M];
                 float lam2s = CUDART_INF_F;            // λ1² of the kRs power iteration
                 if constexpr (kRs) {
-                    n_pow = power_iteration_smem<M, kThreads, true>(Rd, Rs, u, pow_ok, &lam2s);
+                    n_pow = power_iteration_smem<M, kThreads, true>(Rd, Rs, u, pow_ok, &lam2s,
+                                                            (fl & kFlagBorder) ? kPowerTolBorder : kPowerTol);
                     if constexpr (!FB && M >= kWeakTightMinM)
                         if (lam2s < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
                 }
@@ -1131,6 +1162,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                         }
                     }
                     float lam2 = CUDART_INF_F;   // ‖R u‖² of the converged step (λ1²); set at the break only
+                    const float ptol = (fl & kFlagBorder) ? kPowerTolBorder : kPowerTol;
                     for (n_pow = 0; n_pow < kPowerMaxIt;) {
                         // y = R u with R Hermitian: y_i = Rd_i u_i + Σ_{j<i} R_ij u_j + Σ_{j>i} conj(R_ji) u_j
                         cx2 uj[M];
@@ -1164,7 +1196,7 @@ demod_kernel(const float2* __restrict__ frames, int n_frames, int H, int W,
                             u[i] = yn;
                         }
                         ++n_pow;
-                        if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
+                        if (diff < ptol) { pow_ok = true; lam2 = nrm2; break; }
                     }
                     if constexpr (!newton_stop<FB, M>()) {  // weak-tone window (see newton_stop); a flag bit, not a register
                         if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;

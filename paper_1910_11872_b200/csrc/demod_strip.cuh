@@ -140,7 +140,7 @@ __device__ __forceinline__ void strip_load_carry(float (&Rd)[M], cx2 (&Ro)[M * (
 // lam2 = ‖R u‖² of the converged step (λ1²), +inf when the cap was hit.
 template <int M>
 __device__ __forceinline__ int strip_power_iteration(const float (&Rd)[M], const cx2 (&Ro)[M * (M - 1) / 2],
-                                                     cx2 (&u)[M], bool& ok, float& lam2) {
+                                                     cx2 (&u)[M], bool& ok, float& lam2, float tol) {
     float2 r1 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i + 1 < M; ++i) r1 = cadd(r1, cx2_f2(Ro[tri_off<M>(i + 1, i)]));
@@ -189,7 +189,7 @@ __device__ __forceinline__ int strip_power_iteration(const float (&Rd)[M], const
             u[i] = yn;
         }
         ++n;
-        if (diff < kPowerTol) { ok = true; lam2 = nrm2; break; }
+        if (diff < tol) { ok = true; lam2 = nrm2; break; }
     }
     return n;
 }
@@ -305,7 +305,7 @@ demod_strip_kernel(const float2* __restrict__ frames, int n_frames, int H, int W
                     cx2 u[M];
                     bool pow_ok = false;
                     float lam2;
-                    n_pow = strip_power_iteration<M>(Rd, Ro, u, pow_ok, lam2);
+                    n_pow = strip_power_iteration<M>(Rd, Ro, u, pow_ok, lam2, (fl & kFlagBorder) ? kPowerTolBorder : kPowerTol);
                     if constexpr (!newton_stop<false, M>()) {
                         if (lam2 < kWeakNewtonRatio * kWeakNewtonRatio * trace * trace) fl |= kFlagWeakInternal;
                     } else if constexpr (M >= kWeakTightMinM) {
@@ -494,6 +494,7 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                     bool pow_ok = false;
                     float lam2 = CUDART_INF_F;
                     float prev_diff = CUDART_INF_F;
+                    const float ptol = (fl & kFlagBorder) ? kPowerTolBorder : kPowerTol;
                     for (n_pow = 0; n_pow < kPowerMaxIt;) {
                         im_gamma_h<M, TW>(win, u, Vs);                 // t = Γ^H u → slice
                         cx2 t[M], tj[M];
@@ -529,7 +530,7 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                             u[i] = yn;
                         }
                         ++n_pow;
-                        if (diff < kPowerTol) { pow_ok = true; lam2 = nrm2; break; }
+                        if (diff < ptol) { pow_ok = true; lam2 = nrm2; break; }
                         // error-based stop: in the asymptotic regime the step shrinks by ρ = λ2/λ1
                         // per iteration (ρ² ≈ diff/prev_diff) and the remaining error is
                         // ≈ ‖Δu‖·ρ/(1−ρ); stop once that is below kPowerErrTol^½ with ρ ≤ ½.
@@ -539,7 +540,7 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                         // slowest lane's 3rd iteration, so the rule starts at M = 20).
                         if constexpr (M >= kPowerErrStopMinM) {
                             const float r2 = diff / prev_diff;   // 0 after the first iteration (prev = ∞)
-                            if (n_pow >= 2 && r2 < 0.25f) {
+                            if (n_pow >= 2 && r2 < 0.25f && !(fl & kFlagBorder)) {
                                 const float rr = sqrtf(r2);
                                 if (diff * r2 < kPowerErrTol * (1.0f - rr) * (1.0f - rr)) { pow_ok = true; lam2 = nrm2; break; }
                             }
@@ -567,6 +568,295 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                             for (int i = 0; i < M; ++i) q[i] = cx2_f2(Q[i * 32]);
                         },
                         trace, pow_ok, fl, n_aby, n_abx, zx, zy);
+                    if (omx != nullptr) wx = -atan2f(zx.y, zx.x);
+                    if (omy != nullptr) wy = atan2f(zy.y, zy.x);
+                    if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);
+                    if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
+                    if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
+                    result = a;
+                }
+                const size_t o = (size_t)f * plane + (size_t)py * W + px;
+                out[o] = result;
+                if (flags != nullptr) flags[o] = fl & uint8_t(~kFlagWeakInternal);
+                if (omx != nullptr) omx[o] = wx;
+                if (omy != nullptr) omy[o] = wy;
+                if (COUNT) {
+                    atomicAdd(counters + 0, 1ull);
+                    atomicAdd(counters + 1, (unsigned long long)n_pow);
+                    atomicAdd(counters + 2, (unsigned long long)n_aby);
+                    atomicAdd(counters + 3, (unsigned long long)n_abx);
+                }
+            }
+        }
+        cp_async_wait_all();
+    }
+}
+
+
+// ---- Row f4, forward–backward averaging (BOS_VARIANT_FB, [R13]; not in the paper) on the
+// implicit strip kernel: the FB-averaged R_y and S = Γ_w^TΓ_w* = conj(R_x) are never formed;
+// their matvecs run from the tile:
+//   FB(R_y) u = ½[Γ(Γ^H u) + J Γ*(Γ^T (J u))],   FB(S) w = ½[Γ^T(Γ* w) + J Γ^H(Γ (J w))]
+// (J the exchange matrix), four window passes per matvec.  As the row / warp kernels' FB path:
+// two power-iteration starts per axis (tone, ramp-weighted tone; the larger ‖Au‖ wins, the
+// second skipped once λ > ½ tr), u_1 = the FB(R_y) eigenvector, v_1 = conj(the FB(S) one),
+// then the paper's rooting and Eq.(15); weak-tone windows (λ1 < kLowSnrRatio·tr) start the
+// rooting from the tight tolerance (the warp kernel's FB rule).  Parity vs the FP64 oracle's
+// FB variant (tests/test_gpu_strip.py, tools/stress_parity.py --variant fb).
+#ifndef BOS_STRIP_FB_MIN_M
+#define BOS_STRIP_FB_MIN_M 11
+#endif
+constexpr int kStripFbMinM = BOS_STRIP_FB_MIN_M;
+
+template <int M>
+constexpr size_t strip_imfb_smem_bytes() {    // one warp: tile + 3 M-vectors per lane (u, v, scratch)
+    return (size_t)(M + 1) * (32 + M - 1) * sizeof(float2) + (size_t)32 * 3 * M * sizeof(cx2);
+}
+
+// T[k] = Σ_i g(i,k)·a_i, or Σ_i conj(g(i,k))·a_i (CONJ) — column sums, a indexed by row
+template <int M, int TW, bool CONJ>
+__device__ __forceinline__ void im_colsum(const float2* win, const cx2 (&a)[M], cx2* T) {
+    cx2 aj[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i)       // CONJ: −j·a (conj(g)a = gx·a + gy·(−ja));  else j·a
+        aj[i] = CONJ ? mul2(cx2_make(cx2_im(a[i]), cx2_re(a[i])), cx2_make(1.0f, -1.0f))
+                     : mul2(cx2_make(cx2_im(a[i]), cx2_re(a[i])), cx2_make(-1.0f, 1.0f));
+#pragma unroll 1
+    for (int k = 0; k < M; ++k) {
+        cx2 acc = 0ull;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float2 g = win[i * TW + k];
+            acc = fma2(cx2_bcast(g.x), a[i], fma2(cx2_bcast(g.y), aj[i], acc));
+        }
+        T[k * 32] = acc;
+    }
+}
+// Y[i] = Σ_k g(i,k)·t_k, or Σ_k conj(g(i,k))·t_k (CONJ) — row sums, t indexed by column
+template <int M, int TW, bool CONJ>
+__device__ __forceinline__ void im_rowsum(const float2* win, const cx2 (&t)[M], cx2* Y) {
+    cx2 tj[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+        tj[k] = CONJ ? mul2(cx2_make(cx2_im(t[k]), cx2_re(t[k])), cx2_make(1.0f, -1.0f))
+                     : mul2(cx2_make(cx2_im(t[k]), cx2_re(t[k])), cx2_make(-1.0f, 1.0f));
+#pragma unroll 1
+    for (int i = 0; i < M; ++i) {
+        cx2 acc = 0ull;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            const float2 g = win[i * TW + k];
+            acc = fma2(cx2_bcast(g.x), t[k], fma2(cx2_bcast(g.y), tj[k], acc));
+        }
+        Y[i * 32] = acc;
+    }
+}
+template <int M>
+__device__ __forceinline__ void slice_load(const cx2* S, cx2 (&v)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = S[i * 32];
+}
+
+// y = FB(R_y) u (AXIS 0) or FB(S) u (AXIS 1), through the scratch slice T
+template <int M, int TW, int AXIS>
+__device__ __forceinline__ void fb_apply(const float2* win, const cx2 (&u)[M], cx2* T, cx2 (&y)[M]) {
+    cx2 a[M];
+    if constexpr (AXIS == 0) {
+        im_colsum<M, TW, true>(win, u, T);     // Γ^H u
+        slice_load<M>(T, a);
+        im_rowsum<M, TW, false>(win, a, T);    // Γ(Γ^H u)
+        slice_load<M>(T, y);
+#pragma unroll
+        for (int i = 0; i < M; ++i) a[i] = u[M - 1 - i];
+        im_colsum<M, TW, false>(win, a, T);    // Γ^T (J u)
+        slice_load<M>(T, a);
+        im_rowsum<M, TW, true>(win, a, T);     // Γ*(Γ^T J u)
+    } else {
+        im_rowsum<M, TW, true>(win, u, T);     // Γ* w
+        slice_load<M>(T, a);
+        im_colsum<M, TW, false>(win, a, T);    // Γ^T(Γ* w)
+        slice_load<M>(T, y);
+#pragma unroll
+        for (int k = 0; k < M; ++k) a[k] = u[M - 1 - k];
+        im_rowsum<M, TW, false>(win, a, T);    // Γ (J w)
+        slice_load<M>(T, a);
+        im_colsum<M, TW, true>(win, a, T);     // Γ^H(Γ J w)
+    }
+    slice_load<M>(T, a);
+#pragma unroll
+    for (int i = 0; i < M; ++i) y[i] = mul2(add2(y[i], a[M - 1 - i]), cx2_bcast(0.5f));
+}
+
+// power iteration on the FB operator of AXIS from the tone e^{jω̂ i} (RAMP: weighted by
+// i − (M−1)/2), stop at ‖Δu‖² < kPowerTol; lam = ‖A u‖ of the last step
+template <int M, int TW, int AXIS, bool RAMP>
+__device__ __forceinline__ int fb_power(const float2* win, float2 e, cx2* T, cx2 (&u)[M], bool& ok, float& lam) {
+    {
+        const float s0 = RAMP ? rsqrtf(float(M) * float(M * M - 1) / 12.0f) : rsqrtf(float(M));
+        float2 t = make_float2(1.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float wgt = RAMP ? s0 * (float(i) - 0.5f * float(M - 1)) : s0;
+            u[i] = cx2_make(wgt * t.x, wgt * t.y);
+            t = cmul(t, e);
+        }
+    }
+    ok = false;
+    lam = 0.0f;
+    int n = 0;
+#pragma unroll 1
+    for (; n < kPowerMaxIt;) {
+        cx2 y[M];
+        fb_apply<M, TW, AXIS>(win, u, T, y);
+        float nrm2 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) nrm2 += cabs2(cx2_f2(y[i]));
+        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+        lam = sqrtf(nrm2);
+        float diff = 0.0f;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const cx2 yn = mul2(y[i], inv);
+            diff += cabs2(cx2_f2(sub2(yn, u[i])));
+            u[i] = yn;
+        }
+        ++n;
+        if (diff < kPowerTol) { ok = true; break; }
+    }
+    return n;
+}
+
+// dominant eigenvector of the FB operator of AXIS, two starts (see above) → slice OUT
+template <int M, int TW, int AXIS>
+__device__ __forceinline__ int fb_eigvec(const float2* win, float2 e, float trace, cx2* T, cx2* OUT, bool& ok,
+                                         float& lam) {
+    cx2 u[M];
+    int n = fb_power<M, TW, AXIS, false>(win, e, T, u, ok, lam);
+#pragma unroll
+    for (int i = 0; i < M; ++i) OUT[i * 32] = u[i];
+    if (ok && lam > 0.5005f * trace) return n;       // > half the trace of a PSD operator: the top one
+    bool ok2 = false;
+    float lam2 = 0.0f;
+    n += fb_power<M, TW, AXIS, true>(win, e, T, u, ok2, lam2);
+    if (lam2 > lam) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) OUT[i * 32] = u[i];
+        ok = ok2;
+        lam = lam2;
+    }
+    return n;
+}
+
+template <int M, bool COUNT>
+__global__ void __launch_bounds__(32, 8)
+demod_strip_imfb_kernel(const float2* __restrict__ frames, int n_frames, int H, int W, int S,
+                        const float* __restrict__ ref, float* __restrict__ out, uint8_t* __restrict__ flags,
+                        float* __restrict__ omx, float* __restrict__ omy, unsigned long long* __restrict__ counters) {
+    constexpr int O0 = (M - 1) / 2;
+    constexpr int TW = kBX + M - 1;
+    extern __shared__ __align__(16) unsigned char strip_smem[];
+    const int lane = threadIdx.x;
+    float2* tile = reinterpret_cast<float2*>(strip_smem);
+    cx2* Us = reinterpret_cast<cx2*>(tile + (M + 1) * TW) + lane;
+    cx2* Vs = Us + M * 32;
+    cx2* Ts = Vs + M * 32;
+    const size_t plane = (size_t)H * (size_t)W;
+    const int nbx = (W + kBX - 1) / kBX;
+    const int nstrip = (H + S - 1) / S;
+    const long long items = (long long)n_frames * nstrip * nbx;
+
+    for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+        const int bx = (int)(item % nbx);
+        const long long rest = item / nbx;
+        const int f = (int)(rest / nstrip);
+        const int py0 = (int)(rest % nstrip) * S;
+        const int rows = min(S, H - py0);
+        const int x0 = bx * kBX, px = x0 + lane;
+        const float2* __restrict__ frame = frames + (size_t)f * plane;
+        const int gx0 = min(max(x0 - O0 + lane, 0), W - 1);
+        const int gx1 = min(max(x0 - O0 + lane + kBX, 0), W - 1);
+        auto load_row = [&](int r, float2* dst) {
+            const float2* __restrict__ row = frame + (size_t)min(max(py0 - O0 + r, 0), H - 1) * W;
+            cp_async8(dst + lane, row + gx0);
+            if (lane + kBX < TW) cp_async8(dst + lane + kBX, row + gx1);
+        };
+        __syncwarp();
+#pragma unroll 1
+        for (int r = 0; r < M; ++r) load_row(r, tile + r * TW);
+        cp_async_commit();
+        for (int s = 0; s < rows; ++s) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (s > 0) {
+#pragma unroll 1
+                for (int r = 0; r < M; ++r) {
+                    tile[r * TW + lane] = tile[(r + 1) * TW + lane];
+                    if (lane + kBX < TW) tile[r * TW + lane + kBX] = tile[(r + 1) * TW + lane + kBX];
+                }
+                __syncwarp();
+            }
+            if (s + 1 < rows) load_row(s + M, tile + M * TW);
+            cp_async_commit();
+
+            const int py = py0 + s;
+            if (px < W) {
+                const float2* win = tile + lane;
+                uint8_t fl = 0;
+                if (py - O0 < 0 || py + (M - 1 - O0) > H - 1 || px - O0 < 0 || px + (M - 1 - O0) > W - 1)
+                    fl |= kFlagBorder;
+                // tr = ‖Γ_w‖_F²; lag-1 sums of R_y (Σ_i R[i+1][i]) and of S (Σ_k S[k+1][k]) — FB
+                // averaging leaves both unchanged, so they seed the tone starts of both axes
+                float trace = 0.0f;
+                float2 r1y = make_float2(0.0f, 0.0f), r1x = make_float2(0.0f, 0.0f);
+                {
+                    float2 prev[M];
+#pragma unroll
+                    for (int k = 0; k < M; ++k) {
+                        prev[k] = win[k];
+                        trace = fmaf(prev[k].x, prev[k].x, fmaf(prev[k].y, prev[k].y, trace));
+                        if (k > 0) r1x = cfmac(prev[k], prev[k - 1], r1x);
+                    }
+#pragma unroll 1
+                    for (int i = 1; i < M; ++i) {
+                        float2 ry = make_float2(0.0f, 0.0f), rx = make_float2(0.0f, 0.0f);
+                        float2 gl = make_float2(0.0f, 0.0f);
+#pragma unroll
+                        for (int k = 0; k < M; ++k) {
+                            const float2 g = win[i * TW + k];
+                            trace = fmaf(g.x, g.x, fmaf(g.y, g.y, trace));
+                            ry = cfmac(g, prev[k], ry);                // g·conj(row above)
+                            if (k > 0) rx = cfmac(g, gl, rx);          // g·conj(left neighbour)
+                            gl = g;
+                            prev[k] = g;
+                        }
+                        r1y = cadd(r1y, ry);
+                        r1x = cadd(r1x, rx);
+                    }
+                }
+                float result, wx = CUDART_NAN_F, wy = CUDART_NAN_F;
+                int n_pow = 0, n_aby = 0, n_abx = 0;
+                if (!isfinite(trace)) {
+                    fl |= kFlagNonfinite;
+                    result = CUDART_NAN_F;
+                } else {
+                    const float2 ey = cabs2(r1y) > 0.0f ? cscale(r1y, rsqrtf(cabs2(r1y))) : make_float2(1.0f, 0.0f);
+                    const float2 ex = cabs2(r1x) > 0.0f ? cscale(r1x, rsqrtf(cabs2(r1x))) : make_float2(1.0f, 0.0f);
+                    bool oky = false, okx = false;
+                    float lamy = 0.0f, lamx = 0.0f;
+                    n_pow = fb_eigvec<M, TW, 0>(win, ey, trace, Ts, Us, oky, lamy);
+                    n_pow += fb_eigvec<M, TW, 1>(win, ex, trace, Ts, Vs, okx, lamx);
+#pragma unroll 1
+                    for (int k = 0; k < M; ++k) Vs[k * 32] = mul2(Vs[k * 32], cx2_make(1.0f, -1.0f));   // v_1 = conj
+                    if constexpr (M >= kWeakTightMinM)
+                        if (lamy < kLowSnrRatio * trace) fl |= kFlagWeakInternal;
+                    float2 zx, zy;
+                    auto qfn = [&](int axis, float2 (&q)[M]) {
+                        const cx2* Q = axis ? Vs : Us;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) q[i] = cx2_f2(Q[i * 32]);
+                    };
+                    float a = roots_and_phase_q<M, TW, true, (M >= kWeakTightMinM), decltype(qfn)&>(
+                        win, qfn, trace, oky && okx, fl, n_aby, n_abx, zx, zy);
                     if (omx != nullptr) wx = -atan2f(zx.y, zx.x);
                     if (omy != nullptr) wy = atan2f(zy.y, zy.x);
                     if (ref != nullptr) a -= __ldg(ref + (size_t)py * W + px);

@@ -48,3 +48,25 @@ def test_stress_regression_variant(variant, idx):
     mx, rms, nan, exc = run_case(k)
     assert nan == 0, k
     assert rms <= 1e-3 and mx <= 1e-2, (k, mx, rms)
+
+
+# round 2, held-out seeds (tools/stress_r02_regressions.jsonl): M = 4 at −5 dB (an approximation
+# pair sharing one root: 1.39 rad) and M = 32 at 10 dB on a clamped border window (0.063 rad) —
+# loose-stop misplacements, fixed by the per-M loose tolerance (demod_kernel.cuh aberth_tol2);
+# M = 17 at −5 dB in a frame corner (0.0112 rad) — the 1e-8 power-iteration stop, fixed by
+# iterating border windows to FP32 noise (kPowerTolBorder).  Run on both kernel choices.
+R02_CASES = [(103, 151), (104, 7), (106, 21)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,idx", R02_CASES)
+@pytest.mark.parametrize("kernel", ["auto", "strip"])
+def test_stress_regression_round2(seed, idx, kernel, monkeypatch):
+    if kernel == "strip":
+        monkeypatch.setenv("BOS_THREAD_KERNEL", "strip")
+    else:
+        monkeypatch.delenv("BOS_THREAD_KERNEL", raising=False)
+    k = _case(seed, idx)
+    mx, rms, nan, exc = run_case(k)
+    assert nan == 0, k
+    assert rms <= 1e-3 and mx <= 1e-2, (k, mx, rms)
