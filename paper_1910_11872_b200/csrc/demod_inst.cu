@@ -83,7 +83,7 @@ cudaError_t launch_demod(const float2* frames, int n_frames, int H, int W, const
                          uint8_t* flags, float* omega_x, float* omega_y, unsigned long long* counters,
                          cudaStream_t s) {
     const dim3 block(kBX, kBY, 1);
-    constexpr int kKind = FB ? (M >= kStripFbMinM ? 3 : 0) : strip_kind<M>();
+    constexpr int kKind = FB ? ((M >= kStripFbMinM && M <= kStripFbMaxM) ? 3 : 0) : strip_kind<M>();
     if constexpr (kKind > 0) {
         // paper path: the strip kernels (demod_strip.cuh); small launches fall through.  The
         // counting variant (COUNT) takes the same route, so the iteration counts of the flop

@@ -603,10 +603,17 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
 // then the paper's rooting and Eq.(15); weak-tone windows (λ1 < kLowSnrRatio·tr) start the
 // rooting from the tight tolerance (the warp kernel's FB rule).  Parity vs the FP64 oracle's
 // FB variant (tests/test_gpu_strip.py, tools/stress_parity.py --variant fb).
+// measured on C3 1024² ×8 at 10 dB (Mpixel/s, FB implicit strip vs the row / warp kernels):
+// M = 11 818 vs 1220, 16 320 vs 343, 20 223 vs 74, 24 119 vs 55, 26 92 vs 48, 28 51 vs 43, 32 19 vs 32
+// (it spills from M = 22)
 #ifndef BOS_STRIP_FB_MIN_M
-#define BOS_STRIP_FB_MIN_M 11
+#define BOS_STRIP_FB_MIN_M 17
+#endif
+#ifndef BOS_STRIP_FB_MAX_M
+#define BOS_STRIP_FB_MAX_M 28
 #endif
 constexpr int kStripFbMinM = BOS_STRIP_FB_MIN_M;
+constexpr int kStripFbMaxM = BOS_STRIP_FB_MAX_M;
 
 template <int M>
 constexpr size_t strip_imfb_smem_bytes() {    // one warp: tile + 3 M-vectors per lane (u, v, scratch)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--tag", default=os.environ.get("BOS_LIBRARY", "default"))
     ap.add_argument("--workload", default="C3")
+    ap.add_argument("--variant", default="paper", choices=["paper", "fb"])
     a = ap.parse_args()
     dev = torch.device("cuda")
     bosrm.lib()
@@ -37,18 +38,25 @@ def main():
             ref = bosrm.bos_rootmusic_demod(st[:1], M)[0][0]
             fr = st[1:]
             out = torch.empty(fr.shape, dtype=torch.float32, device=dev)
-            bosrm.bos_rootmusic_demod(fr, M, ref_phase=ref, out_phase=out)
+            if a.variant == "fb":
+                def run():
+                    bosrm.bos_rootmusic_demod_variant(fr, M, variant=bosrm.VARIANT_FB, ref_phase=ref, out_phase=out)
+            else:
+                def run():
+                    bosrm.bos_rootmusic_demod(fr, M, ref_phase=ref, out_phase=out)
+            run()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(a.reps):
-                bosrm.bos_rootmusic_demod(fr, M, ref_phase=ref, out_phase=out)
+                run()
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
-            c = bosrm.bos_rootmusic_iteration_counts(fr[:4], M, ref_phase=ref)
+            c = bosrm.bos_rootmusic_iteration_counts(fr[:4], M, ref_phase=ref) if a.variant == "paper" else \
+                dict(pixels=1, power_its=0, aberth_y=0, aberth_x=0)
             n = max(1, c["pixels"])
-            print(json.dumps({"tag": a.tag, "M": M, "snr": snr, "mpix_s": round(fr.numel() / ms / 1e3, 1),
+            print(json.dumps({"tag": a.tag, "variant": a.variant, "M": M, "snr": snr, "mpix_s": round(fr.numel() / ms / 1e3, 1),
                               "ms": round(ms, 3), "power": round(c["power_its"] / n, 3),
                               "aby": round(c["aberth_y"] / n, 3), "abx": round(c["aberth_x"] / n, 3)}), flush=True)
             del out
