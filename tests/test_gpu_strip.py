@@ -118,3 +118,21 @@ def test_strip_kernels_minimum_and_thin_frames(M, monkeypatch):
             b = _run(fr.to(DEV), M, monkeypatch, row=True)
             a = _run(fr.to(DEV), M, monkeypatch, row=False)
             _assert_same(a, b, f"M={M} {H}x{W}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M", [17, 20, 24, 28])
+def test_strip_fb_kernel_parity(M, monkeypatch):
+    """Row f4's forward–backward variant on the implicit strip kernel (M = 17…28): FB(R_y) and
+    FB(S) applied from the tile, two starts per axis — parity with the oracle's FB variant
+    ([R13]) on a ragged 10 dB and a 0 dB frame, and validity of the excluded pixels."""
+    monkeypatch.setenv("BOS_THREAD_KERNEL", "strip")
+    w = synth.workload("C3", H=M + 29, W=M + 45, seed=19)
+    for t, snr in ((2, 10.0), (3, 0.0)):
+        f = synth.make_frame(w, t, snr_db=snr)
+        g, gfl, wx, wy = bosrm.bos_rootmusic_demod_variant(f.unsqueeze(0).to(DEV), M, variant=bosrm.VARIANT_FB,
+                                                            flags=True, omega=True)
+        g, gfl, wx, wy = (x[0].cpu().numpy() for x in (g, gfl, wx, wy))
+        o, ofl = R.demod_frame(f.numpy(), M, variant="fb")
+        assert_parity(g, o, ofl, f"strip FB M={M} {snr} dB", gpu_flags=gfl)
+        assert_excluded_valid(f.numpy(), M, g, wx, wy, ofl, f"strip FB M={M} {snr} dB", variant="fb")
