@@ -188,7 +188,8 @@ int bos_rootmusic_demod_ex(const bos_cf32* frames, int n_frames, int H, int W,
  *            device memory free, or lower it afterwards with cudaDeviceSetLimit(
  *            cudaLimitStackSize, …) once the call has completed.
  *            Any other bit: BOS_ERR_UNSUPPORTED.
- * The FP32 variants run the hot path's kernels (demod_kernel.cuh, demod_wide.cuh; smoothing:
+ * The FP32 variants run the hot path's kernels (FB: demod_kernel.cuh up to M = 16, the implicit
+ * strip kernel demod_strip.cuh for 17…28, demod_wide.cuh beyond; smoothing:
  * demod_ss.cuh); FP64 runs demod_f64.cuh.  Other arguments, errors and determinism as
  * bos_rootmusic_demod_ex.
  */
