@@ -231,7 +231,10 @@ __device__ __forceinline__ int edge_k(const float* __restrict__ w, int a, int b)
 #ifndef BOS_UNWRAP_TILE
 #define BOS_UNWRAP_TILE 16
 #endif
-constexpr int kTile = BOS_UNWRAP_TILE;       // 16: 256-thread CTAs, 8 per SM (32: one 1024-thread CTA per SM — its barriers stall the SM — 14.2 ms of 23.8 per 100 1024² frames)
+constexpr int kTile = BOS_UNWRAP_TILE;
+#ifndef BOS_UNWRAP_TILE_ROUNDS
+#define BOS_UNWRAP_TILE_ROUNDS 32   // local Borůvka rounds (the global rounds finish whatever is left)
+#endif       // 16: 256-thread CTAs, 8 per SM (32: one 1024-thread CTA per SM — its barriers stall the SM — 14.2 ms of 23.8 per 100 1024² frames)
 __device__ __forceinline__ unsigned tpk(int parent, int off) { return (unsigned)(parent & 0xffff) | ((unsigned)off << 16); }
 __device__ __forceinline__ int tpar(unsigned v) { return (int)(v & 0xffffu); }
 __device__ __forceinline__ int tofs(unsigned v) { return (int)v >> 16; }
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
         if (y > 0)     { has |= 8u; eid[3] = 2u * (unsigned)(p - W) + 1u; ol[3] = ly > 0 ? l - kTile : -1;         key[3] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - W], rp)); }
     }
     __syncthreads();
-    for (int round = 0; round < 32; ++round) {
+    for (int round = 0; round < BOS_UNWRAP_TILE_ROUNDS; ++round) {
         const int r = tpar(node[l]);                        // fully compressed: the root
         bkey[l] = 0ull;
         bid[l] = 0xffffffffu;
