@@ -57,6 +57,10 @@ constexpr int strip_kind() {
 #define BOS_POWER_ERR_TOL 1e-10f // squared estimated eigenvector error at the error-based stop
 #endif
 constexpr int kPowerErrStopMinM = BOS_POWER_ERR_STOP_MIN_M;
+#ifndef BOS_POWER_SHIFT
+#define BOS_POWER_SHIFT 0        // implicit strip kernel: shifted power iteration (see there)
+#endif
+constexpr bool kPowerShift = BOS_POWER_SHIFT != 0;
 constexpr float kPowerErrTol = BOS_POWER_ERR_TOL;
 #ifndef BOS_STRIP_ROWS
 #define BOS_STRIP_ROWS 16        // S: rows per work item (fewer for small launches, see launch_strip)
@@ -515,13 +519,29 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                             Vs[i * 32] = acc;
                         }
                         cx2 y[M];
-                        float nrm2 = 0.0f;
+                        float nrm2 = 0.0f, rq = 0.0f;            // ‖R u‖², Rayleigh quotient u^H R u
 #pragma unroll
                         for (int i = 0; i < M; ++i) {
                             y[i] = Vs[i * 32];
                             nrm2 += cabs2(cx2_f2(y[i]));
+                            rq = fmaf(cx2_re(u[i]), cx2_re(y[i]), fmaf(cx2_im(u[i]), cx2_im(y[i]), rq));
                         }
-                        const cx2 inv = cx2_bcast(rsqrtf(nrm2));
+                        // shifted step (R − μI)u with μ = the mean of the other eigenvalues,
+                        // (tr − λ1)/(M−1), once λ1 > 3μ: the step ratio (λ2 − μ)/(λ1 − μ) instead of
+                        // λ2/λ1 — fewer iterations for weak-tone windows; same eigenvector
+                        float nrm2s = nrm2;
+                        if constexpr (kPowerShift) {
+                            const float mu = (trace - rq) * (1.0f / float(M - 1));
+                            if (rq > 3.0f * mu && mu > 0.0f) {
+                                nrm2s = 0.0f;
+#pragma unroll
+                                for (int i = 0; i < M; ++i) {
+                                    y[i] = fma2(cx2_bcast(-mu), u[i], y[i]);
+                                    nrm2s += cabs2(cx2_f2(y[i]));
+                                }
+                            }
+                        }
+                        const cx2 inv = cx2_bcast(rsqrtf(nrm2s));
                         float diff = 0.0f;
 #pragma unroll
                         for (int i = 0; i < M; ++i) {
