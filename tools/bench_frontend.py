@@ -23,9 +23,12 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--window-len", type=int, default=8)
+    ap.add_argument("--height", type=int, default=None, help="frame height (default --size)")
+    ap.add_argument("--width", type=int, default=None, help="frame width (default --size); the paper's "
+                    "experiment: --frames 19 --height 700 --width 1850 --window-len 15 (P:L386-389)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    w = synth.workload("C3", H=args.size, W=args.size)
+    w = synth.workload("C3", H=args.height or args.size, W=args.width or args.size)
     T = args.frames
     u8 = torch.stack([synth.make_intensity_frame(w, t, device=dev) for t in range(T)])
     gamma = torch.empty(T, w.H, w.W, dtype=torch.complex64, device=dev)
