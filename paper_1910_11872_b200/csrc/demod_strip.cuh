@@ -357,9 +357,20 @@ demod_strip_kernel(const float2* __restrict__ frames, int n_frames, int H, int W
 // the kernel's code — and its instruction-cache footprint — O(M) instead of O(M²).
 // Same FP32 chain otherwise; parity against the FP64 oracle (tests/test_gpu_strip.py).
 
+// M-vectors per lane the implicit kernel keeps in shared memory.  2: u_1 and v_1 in two
+// slices.  1 (M ≥ BOS_STRIP_IM_ONE_SLOT_MIN_M): one slice holds the power iteration's scratch,
+// then u_1; v_1 = Γ_w^H u_1/‖·‖ is formed in registers when the x axis starts (u_1 is dead by
+// then) — 8 KB less per warp at M = 32, which lifts the SM from 6 to 8 resident warps at
+// M = 31, 32 (measured +8 % at M = 32, 10 and 0 dB; at M = 30 — 7 → 8 warps — −3 %…0, so the
+// two-slice layout stays below).
+#ifndef BOS_STRIP_IM_ONE_SLOT_MIN_M
+#define BOS_STRIP_IM_ONE_SLOT_MIN_M 31
+#endif
 template <int M>
-constexpr size_t strip_im_smem_bytes() {      // one warp: tile (M+1 rows) + 2 M-vectors per lane
-    return (size_t)(M + 1) * (32 + M - 1) * sizeof(float2) + (size_t)32 * 2 * M * sizeof(cx2);
+constexpr int strip_im_slots() { return M >= BOS_STRIP_IM_ONE_SLOT_MIN_M ? 1 : 2; }
+template <int M>
+constexpr size_t strip_im_smem_bytes() {      // one warp: tile (M+1 rows) + strip_im_slots M-vectors per lane
+    return (size_t)(M + 1) * (32 + M - 1) * sizeof(float2) + (size_t)32 * strip_im_slots<M>() * M * sizeof(cx2);
 }
 
 // t = Γ_w^H u column by column (t_k = Σ_i conj(Γ(i,k)) u_i, v1_from_window's arithmetic) into
@@ -382,6 +393,30 @@ __device__ __forceinline__ float im_gamma_h(const float2* win, const cx2 (&u)[M]
         T[k * 32] = acc;
         n2 += cabs2(cx2_f2(acc));
     }
+    return n2;
+}
+
+// the same t = Γ_w^H u with u read from the slice U one entry per row and t kept in registers
+// (row-outer order: one u_i live instead of u and −j·u; per-k sums in the same order and
+// nesting as im_gamma_h, so bitwise equal); returns ‖t‖²
+template <int M, int TW>
+__device__ __forceinline__ float im_gamma_h_rows(const float2* win, const cx2* U, cx2 (&t)[M]) {
+    const cx2 kPosNeg = cx2_make(1.0f, -1.0f);
+#pragma unroll
+    for (int k = 0; k < M; ++k) t[k] = 0ull;
+#pragma unroll 1
+    for (int i = 0; i < M; ++i) {
+        const cx2 ui = U[i * 32];
+        const cx2 uj = mul2(cx2_make(cx2_im(ui), cx2_re(ui)), kPosNeg);   // −j·u_i
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            const float2 g = win[i * TW + k];
+            t[k] = fma2(cx2_bcast(g.x), ui, fma2(cx2_bcast(g.y), uj, t[k]));
+        }
+    }
+    float n2 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < M; ++k) n2 += cabs2(cx2_f2(t[k]));
     return n2;
 }
 
@@ -409,7 +444,7 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
     const int lane = threadIdx.x;
     float2* tile = reinterpret_cast<float2*>(strip_smem);
     cx2* Us = reinterpret_cast<cx2*>(tile + (M + 1) * TW) + lane;   // u_1: entry i at Us[i·32]
-    cx2* Vs = Us + M * 32;                                         // v_1 (and the iteration's scratch)
+    cx2* Vs = strip_im_slots<M>() == 1 ? Us : Us + M * 32;           // v_1 (and the iteration's scratch)
     const size_t plane = (size_t)H * (size_t)W;
     const int nbx = (W + kBX - 1) / kBX;
     const int nstrip = (H + S - 1) / S;
@@ -569,8 +604,13 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                     }
                     if constexpr (M >= kWeakTightMinM)
                         if (lam2 < kLowSnrRatio * kLowSnrRatio * trace * trace) fl |= kFlagWeakInternal;
-                    // u_1 and v_1 = Γ_w^H u_1/‖·‖ to the slice (v1_from_window's arithmetic)
-                    {
+                    // u_1 and v_1 = Γ_w^H u_1/‖·‖ to the slice(s) (v1_from_window's arithmetic);
+                    // one slice: u_1 now, v_1 formed in registers when the x axis starts
+                    if constexpr (strip_im_slots<M>() == 1) {
+#pragma unroll
+                        for (int k = 0; k < M; ++k) Us[k * 32] = u[k];
+                        compiler_fence();       // no store-to-load forwarding: u must not stay live into the axis loop
+                    } else {
                         const float vn = im_gamma_h<M, TW>(win, u, Vs);
                         const cx2 vinv = cx2_bcast(rsqrtf(vn));
 #pragma unroll
@@ -583,9 +623,22 @@ demod_strip_im_kernel(const float2* __restrict__ frames, int n_frames, int H, in
                     float a = roots_and_phase_q<M, TW, false, (M >= kWeakTightMinM)>(
                         win,
                         [&](int axis, float2 (&q)[M]) {
-                            const cx2* Q = axis ? Vs : Us;
+                            if constexpr (strip_im_slots<M>() == 1) {
+                                if (axis) {
+                                    cx2 t[M];
+                                    const float vn = im_gamma_h_rows<M, TW>(win, Us, t);
+                                    const cx2 vinv = cx2_bcast(rsqrtf(vn));
 #pragma unroll
-                            for (int i = 0; i < M; ++i) q[i] = cx2_f2(Q[i * 32]);
+                                    for (int i = 0; i < M; ++i) q[i] = cx2_f2(mul2(t[i], vinv));
+                                } else {
+#pragma unroll
+                                    for (int i = 0; i < M; ++i) q[i] = cx2_f2(Us[i * 32]);
+                                }
+                            } else {
+                                const cx2* Q = axis ? Vs : Us;
+#pragma unroll
+                                for (int i = 0; i < M; ++i) q[i] = cx2_f2(Q[i * 32]);
+                            }
                         },
                         trace, pow_ok, fl, n_aby, n_abx, zx, zy);
                     if (omx != nullptr) wx = -atan2f(zx.y, zx.x);
