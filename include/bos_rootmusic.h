@@ -130,10 +130,15 @@ size_t bos_rootmusic_host_workspace_bytes(int H, int W, int chunk_frames, int wi
 
 /*
  * bos_rootmusic_demod_stack_host — bos_rootmusic_demod_stack on HOST buffers: the frames
- * are streamed host→device in chunks of chunk_frames, demodulated, and the phases (and
- * flags) streamed back, with the copies of one chunk overlapping the kernels of the
+ * are streamed host→device in chunks of at most chunk_frames, demodulated, and the phases
+ * (and flags) streamed back, with the copies of one chunk overlapping the kernels of the
  * other on two internal streams (created on the first call on a device and reused; see
- * the file header).
+ * the file header).  The reference frame goes first, alone; the other frames follow in
+ * chunks of 1, 2, 4, … up to chunk_frames, halving again over the tail, so the pipeline
+ * fills and drains in about one frame's copy.  Outputs and flags equal
+ * bos_rootmusic_demod_stack's bit for bit wherever both run the same kernel (every window
+ * length except 11 and 14–16, whose small chunks run the row kernel instead of the implicit
+ * strip kernel: equal within the parity tolerance there).
  *   h_frames     HOST [n_frames][H][W] bos_cf32 (pinned for full overlap; pageable works).
  *   h_out_phase  HOST [n_frames][H][W] float32, written.  h_flags: HOST uint8 or NULL.
  *   d_workspace  DEVICE scratch of ≥ bos_rootmusic_host_workspace_bytes(H, W, chunk_frames,

@@ -438,33 +438,57 @@ int bos_rootmusic_demod_stack_host(const bos_cf32* h_frames, int n_frames, int H
         ok(cudaEventRecord(ev_start, user));
         ok(cudaStreamWaitEvent(st[0], ev_start, 0));
         ok(cudaStreamWaitEvent(st[1], ev_start, 0));
-        // reference frame → d_ref (raw α), on stream 0
+        // chunk 0 = the reference frame alone, on stream 0: H2D → raw α → d_ref, its own output
+        // wrap(α_ref − α_ref) by the pointwise kernel (as bos_rootmusic_demod_stack), D2H
         ok(cudaMemcpyAsync(d_frames[0], h_frames + (size_t)ref_index * plane, plane * sizeof(bos_cf32),
                            cudaMemcpyHostToDevice, st[0]));
         if (e == cudaSuccess) {
-            rc = demod_impl(d_frames[0], 1, H, W, window_len, model_order, nullptr, d_ref, nullptr, nullptr, st[0],
-                            false);
+            rc = demod_impl(d_frames[0], 1, H, W, window_len, model_order, nullptr, d_ref, d_flags[0], nullptr,
+                            st[0], false);
             if (rc != BOS_OK && e == cudaSuccess) e = cudaErrorLaunchFailure;
         }
+        if (e == cudaSuccess) {
+            const unsigned blocks = (unsigned)std::min<size_t>((plane + 255) / 256, 148 * 8);
+            self_difference_kernel<<<blocks, 256, 0, st[0]>>>(d_ref, plane, d_out[0]);
+            ok(cudaGetLastError());
+        }
         ok(cudaEventRecord(ev_ref, st[0]));
-        ok(cudaStreamWaitEvent(st[1], ev_ref, 0));
-        // ping-pong chunks: H2D(k) ‖ kernel(k−1) ‖ D2H(k−2) across the two streams
-        for (int f0 = 0, k = 0; f0 < n_frames && e == cudaSuccess; f0 += chunk_frames, ++k) {
-            const int s = k & 1;
-            const int nk = std::min(chunk_frames, n_frames - f0);
-            const size_t cnt = (size_t)nk * plane;
-            ok(cudaMemcpyAsync(d_frames[s], h_frames + (size_t)f0 * plane, cnt * sizeof(bos_cf32),
-                               cudaMemcpyHostToDevice, st[s]));
-            if (e != cudaSuccess) break;
-            rc = demod_impl(d_frames[s], nk, H, W, window_len, model_order, d_ref, d_out[s], d_flags[s], nullptr,
-                            st[s], false);
-            if (rc != BOS_OK) {
-                e = cudaErrorLaunchFailure;
-                break;
+        ok(cudaMemcpyAsync(h_out_phase + (size_t)ref_index * plane, d_out[0], plane * sizeof(float),
+                           cudaMemcpyDeviceToHost, st[0]));
+        if (wf) ok(cudaMemcpyAsync(h_flags + (size_t)ref_index * plane, d_flags[0], plane, cudaMemcpyDeviceToHost, st[0]));
+        // the other frames, [0, ref) then (ref, n), in chunks ping-ponged over the two streams
+        // (H2D(k) ‖ kernel(k−1) ‖ D2H(k−2)).  Chunk sizes ramp up 1, 2, 4, … to chunk_frames and
+        // halve again over the tail (never more than half of what is left), so the pipeline
+        // fills and drains in about one frame's copy time instead of a whole chunk's.  Stream 1 starts its first copy before
+        // it waits for the reference phase.
+        bool waited_ref = false;
+        int k = 1, ramp = 1;
+        for (int part = 0; part < 2 && e == cudaSuccess; ++part) {
+            const int lo = part == 0 ? 0 : ref_index + 1, hi = part == 0 ? ref_index : n_frames;
+            for (int f0 = lo; f0 < hi && e == cudaSuccess; ++k) {
+                const int s = k & 1;
+                const int left = hi - f0;
+                const int nk = std::min(std::min(ramp, chunk_frames), std::max(1, (left + 1) / 2));
+                ramp = std::min(2 * ramp, chunk_frames);
+                const size_t cnt = (size_t)nk * plane;
+                ok(cudaMemcpyAsync(d_frames[s], h_frames + (size_t)f0 * plane, cnt * sizeof(bos_cf32),
+                                   cudaMemcpyHostToDevice, st[s]));
+                if (s == 1 && !waited_ref) {
+                    ok(cudaStreamWaitEvent(st[1], ev_ref, 0));
+                    waited_ref = true;
+                }
+                if (e != cudaSuccess) break;
+                rc = demod_impl(d_frames[s], nk, H, W, window_len, model_order, d_ref, d_out[s], d_flags[s],
+                                nullptr, st[s], false);
+                if (rc != BOS_OK) {
+                    e = cudaErrorLaunchFailure;
+                    break;
+                }
+                ok(cudaMemcpyAsync(h_out_phase + (size_t)f0 * plane, d_out[s], cnt * sizeof(float),
+                                   cudaMemcpyDeviceToHost, st[s]));
+                if (wf) ok(cudaMemcpyAsync(h_flags + (size_t)f0 * plane, d_flags[s], cnt, cudaMemcpyDeviceToHost, st[s]));
+                f0 += nk;
             }
-            ok(cudaMemcpyAsync(h_out_phase + (size_t)f0 * plane, d_out[s], cnt * sizeof(float),
-                               cudaMemcpyDeviceToHost, st[s]));
-            if (wf) ok(cudaMemcpyAsync(h_flags + (size_t)f0 * plane, d_flags[s], cnt, cudaMemcpyDeviceToHost, st[s]));
         }
         cudaEventRecord(ev_end[0], st[0]);
         cudaEventRecord(ev_end[1], st[1]);

@@ -35,6 +35,13 @@
 namespace bos {
 
 constexpr int kSweepUnroll = BOS_SWEEP_UNROLL;   // root-update loop unroll factor (A/B builds)
+// the sweep's root loop is unrolled completely for K = N/2 ≤ BOS_SWEEP_FULL_MAX_K roots: the
+// array rotation below then compiles to register renaming (no MOVs) at a code size the
+// instruction cache still holds
+#ifndef BOS_SWEEP_FULL_MAX_K
+#define BOS_SWEEP_FULL_MAX_K 4
+#endif
+constexpr int sweep_unroll(int K) { return K <= BOS_SWEEP_FULL_MAX_K ? K : kSweepUnroll; }
 
 constexpr int kBX = 32;               // pixels per CTA along x (one warp per row)
 constexpr int kBY = 4;                // rows per CTA
@@ -318,7 +325,7 @@ __device__ __forceinline__ int aberth_sym(const cx2 (&c)[N + 1], cx2 (&z)[N / 2]
     for (; it < kAberthMaxIt; ++it) {
         float maxw = 0.0f;
         bool parked = false;               // some |P/P′|² ≥ tol2 (NEWTON_STOP)
-#pragma unroll kSweepUnroll
+#pragma unroll sweep_unroll(K)
         for (int r = 0; r < K; ++r) {
             const float2 zi = cx2_f2(z[0]);
             float2 num, den;                   // Newton ratio P/P′ = num/den

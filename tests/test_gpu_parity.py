@@ -179,6 +179,21 @@ def test_host_api_matches_device_api():
     assert torch.equal(h_out2, dev_out.cpu())
 
 
+@pytest.mark.parametrize("ref_index,chunk,M", [(3, 4, 8), (9, 5, 8), (6, 3, 15), (0, 16, 5)])
+def test_host_api_ramped_chunks(ref_index, chunk, M):
+    """The host pipeline's chunk schedule (the reference frame alone first; the other frames in
+    chunks ramping 1, 2, 4, … up to chunk_frames and halving over the tail, never across the
+    reference) gives the device stack's outputs and flags bit for bit, for any ref_index."""
+    w = synth.workload("C3", H=64, W=96)
+    stack = synth.make_stack(w, frames=range(10), snr_db=5.0)
+    dev_out, dev_fl, dev_ref = bosrm.bos_rootmusic_demod_stack(stack.to(DEV), M, ref_index=ref_index, flags=True)
+    h_out, h_fl = bosrm.bos_rootmusic_demod_stack_host(stack.pin_memory(), M, ref_index=ref_index, h_flags=True,
+                                                      chunk_frames=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.nan_to_num(h_out, 9.0), torch.nan_to_num(dev_out.cpu(), 9.0))
+    assert torch.equal(h_fl, dev_fl.cpu())
+
+
 def test_error_codes_on_device():
     f = torch.zeros(1, 32, 32, dtype=torch.complex64, device=DEV)
     out = torch.empty(1, 32, 32, dtype=torch.float32, device=DEV)
