@@ -239,7 +239,10 @@ __device__ __forceinline__ unsigned tpk(int parent, int off) { return (unsigned)
 __device__ __forceinline__ int tpar(unsigned v) { return (int)(v & 0xffffu); }
 __device__ __forceinline__ int tofs(unsigned v) { return (int)v >> 16; }
 
-__global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_boruvka(const float* __restrict__ w, const double* __restrict__ rel,
+#ifndef BOS_UNWRAP_TILE_MIN_BLOCKS
+#define BOS_UNWRAP_TILE_MIN_BLOCKS (2048 / (kTile * kTile))
+#endif
+__global__ void __launch_bounds__(kTile * kTile, BOS_UNWRAP_TILE_MIN_BLOCKS) tile_boruvka(const float* __restrict__ w, const double* __restrict__ rel,
                                                               int H, int W, int F, unsigned long long* __restrict__ po,
                                                               unsigned* __restrict__ roots, unsigned* __restrict__ roots0,
                                                               unsigned* __restrict__ nroots, unsigned* __restrict__ edges,
@@ -248,6 +251,10 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
     __shared__ unsigned long long bkey[kTile * kTile];       // best incident key per component root
     __shared__ unsigned bid[kTile * kTile];                  // best incident edge id per component root
     __shared__ unsigned staged[kTile * kTile];
+    // this node's 4 incident edges in fixed slots (right, down, left, up): the keys in shared
+    // memory (registers bound the CTAs per SM: 62 registers with them in registers, 4 CTAs);
+    // edge id and local index of the other end (−1: outside the tile) recomputed from p, l
+    __shared__ unsigned long long skey[4][kTile * kTile];
     const int tilesx = (W + kTile - 1) / kTile, tilesy = (H + kTile - 1) / kTile;
     const int f = blockIdx.x / (tilesx * tilesy);
     const int t = blockIdx.x % (tilesx * tilesy);
@@ -258,18 +265,21 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
     const size_t plane = (size_t)H * W;
     const int p = (int)((size_t)f * plane + (size_t)y * W + x);
     node[l] = tpk(l, 0);
-    // this node's 4 incident edges in fixed slots (right, down, left, up): edge id, local index
-    // of the other end (−1: outside the tile), key; `has` = the slots that exist
-    unsigned eid[4] = {0u, 0u, 0u, 0u};
-    int ol[4] = {-1, -1, -1, -1};
-    unsigned long long key[4] = {0ull, 0ull, 0ull, 0ull};
+    auto eid = [&](int k) -> unsigned {
+        return k == 0 ? 2u * (unsigned)p : k == 1 ? 2u * (unsigned)p + 1u : k == 2 ? 2u * (unsigned)(p - 1)
+                                                                                    : 2u * (unsigned)(p - W) + 1u;
+    };
+    auto ol = [&](int k) -> int {
+        return k == 0 ? (lx + 1 < kTile ? l + 1 : -1) : k == 1 ? (ly + 1 < kTile ? l + kTile : -1)
+                                                              : k == 2 ? (lx > 0 ? l - 1 : -1) : (ly > 0 ? l - kTile : -1);
+    };
     unsigned has = 0;
     if (valid) {
         const double rp = rel[p];
-        if (x + 1 < W) { has |= 1u; eid[0] = 2u * (unsigned)p;            ol[0] = lx + 1 < kTile ? l + 1 : -1;     key[0] = (unsigned long long)__double_as_longlong(__dadd_rn(rp, rel[p + 1])); }
-        if (y + 1 < H) { has |= 2u; eid[1] = 2u * (unsigned)p + 1u;       ol[1] = ly + 1 < kTile ? l + kTile : -1; key[1] = (unsigned long long)__double_as_longlong(__dadd_rn(rp, rel[p + W])); }
-        if (x > 0)     { has |= 4u; eid[2] = 2u * (unsigned)(p - 1);      ol[2] = lx > 0 ? l - 1 : -1;             key[2] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - 1], rp)); }
-        if (y > 0)     { has |= 8u; eid[3] = 2u * (unsigned)(p - W) + 1u; ol[3] = ly > 0 ? l - kTile : -1;         key[3] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - W], rp)); }
+        if (x + 1 < W) { has |= 1u; skey[0][l] = (unsigned long long)__double_as_longlong(__dadd_rn(rp, rel[p + 1])); }
+        if (y + 1 < H) { has |= 2u; skey[1][l] = (unsigned long long)__double_as_longlong(__dadd_rn(rp, rel[p + W])); }
+        if (x > 0)     { has |= 4u; skey[2][l] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - 1], rp)); }
+        if (y > 0)     { has |= 8u; skey[3][l] = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p - W], rp)); }
     }
     __syncthreads();
     for (int round = 0; round < BOS_UNWRAP_TILE_ROUNDS; ++round) {
@@ -279,11 +289,11 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (((has >> k) & 1u) && (ol[k] < 0 || tpar(node[ol[k]]) != r)) atomicMax(bkey + r, key[k]);
+            if (((has >> k) & 1u) && (ol(k) < 0 || tpar(node[ol(k)]) != r)) atomicMax(bkey + r, skey[k][l]);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (((has >> k) & 1u) && (ol[k] < 0 || tpar(node[ol[k]]) != r) && key[k] == bkey[r]) atomicMin(bid + r, eid[k]);
+            if (((has >> k) & 1u) && (ol(k) < 0 || tpar(node[ol(k)]) != r) && skey[k][l] == bkey[r]) atomicMin(bid + r, eid(k));
         __syncthreads();
         // roots hook across their best edge when it stays inside the tile; the edge's tile-side
         // end that belongs to this component is p_in, the other end q_out
@@ -331,8 +341,8 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
     __syncthreads();
     const unsigned v = node[l];
     const bool is_root = valid && tpar(v) == l;
-    const bool cr = ((has & 1u) != 0) && (ol[0] < 0 || tpar(node[ol[0]]) != tpar(v));
-    const bool cd = ((has & 2u) != 0) && (ol[1] < 0 || tpar(node[ol[1]]) != tpar(v));
+    const bool cr = ((has & 1u) != 0) && (ol(0) < 0 || tpar(node[ol(0)]) != tpar(v));
+    const bool cd = ((has & 2u) != 0) && (ol(1) < 0 || tpar(node[ol(1)]) != tpar(v));
     const unsigned my_r = is_root ? atomicAdd(&cnt_r, 1u) : 0u;
     const unsigned my_e = (cr || cd) ? atomicAdd(&cnt_e, (unsigned)cr + (unsigned)cd) : 0u;
     __syncthreads();
@@ -345,8 +355,8 @@ __global__ void __launch_bounds__(kTile * kTile, 1024 / (kTile * kTile)) tile_bo
         roots[base_r + my_r] = (unsigned)p;
         roots0[base_r + my_r] = (unsigned)p;
     }
-    if (cr) edges[base_e + my_e] = eid[0];
-    if (cd) edges[base_e + my_e + (cr ? 1u : 0u)] = eid[1];
+    if (cr) edges[base_e + my_e] = eid(0);
+    if (cd) edges[base_e + my_e + (cr ? 1u : 0u)] = eid(1);
     if (valid) {
         const int rl = tpar(v);
         const int gr = (int)((size_t)f * plane + (size_t)(y0 + rl / kTile) * W + (x0 + rl % kTile));
