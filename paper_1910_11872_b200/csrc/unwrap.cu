@@ -232,6 +232,9 @@ __device__ __forceinline__ int edge_k(const float* __restrict__ w, int a, int b)
 #define BOS_UNWRAP_TILE 16
 #endif
 constexpr int kTile = BOS_UNWRAP_TILE;
+#ifndef BOS_UNWRAP_CHASE
+#define BOS_UNWRAP_CHASE 1     // 1: root chains compressed by one chase_list launch; 0: jump_list pairs + readbacks
+#endif
 #ifndef BOS_UNWRAP_TILE_ROUNDS
 #define BOS_UNWRAP_TILE_ROUNDS 32   // local Borůvka rounds (the global rounds finish whatever is left)
 #endif       // 16: 256-thread CTAs, 8 per SM (32: one 1024-thread CTA per SM — its barriers stall the SM — 14.2 ms of 23.8 per 100 1024² frames)
@@ -411,6 +414,7 @@ __global__ void apply_list(const unsigned* __restrict__ list, const unsigned* __
         po[c] = staged[c];
     }
 }
+#if !BOS_UNWRAP_CHASE
 __global__ void jump_list(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
                           unsigned long long* po, int* __restrict__ changed) {
     const unsigned n = *count;
@@ -424,6 +428,33 @@ __global__ void jump_list(const unsigned* __restrict__ list, const unsigned* __r
             po[i] = pk(pp, ofs(wi) + ofs(wp));
             *changed = 1;
         }
+    }
+}
+#endif
+// compress the root chains after a round's hooks in ONE launch: every listed node follows its
+// parent pointers to the root (a hooked root's chain may be several components long) and
+// stores (root, Σ offsets).  Entries other threads rewrite meanwhile are ancestors with the
+// matching offset sums (packed 64-bit words: a reader sees the old or the new pair, both
+// consistent), so every walk ends at the same root with the same sum; the hooks leave no
+// cycle (of a mutual pair the smaller id stays root).  Replaces 2·k jump_list launches and a
+// host readback per two of them.
+__global__ void chase_list(const unsigned* __restrict__ list, const unsigned* __restrict__ count,
+                           unsigned long long* po) {
+    const unsigned n = *count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const unsigned i = list[k];
+        const unsigned long long wi = __ldcg(po + i);
+        int p = par(wi);
+        if (p == (int)i) continue;
+        int off = ofs(wi);
+        for (;;) {
+            const unsigned long long wp = __ldcg(po + p);
+            const int pp = par(wp);
+            if (pp == p) break;
+            off += ofs(wp);
+            p = pp;
+        }
+        po[i] = pk(p, off);
     }
 }
 // every node: (old root r, off) → (root(r), off + off(r)); roots' entries already point at
@@ -618,7 +649,9 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
     const size_t tot = plane * (size_t)n_frames * sizeof(float);
     if (a != b && a < b + tot && b < a + tot) return BOS_ERR_INVALID_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+#if !BOS_UNWRAP_CHASE
     int host_flags[2];
+#endif
     for (int f0 = 0; f0 < n_frames; f0 += F) {
         const int nf = std::min(F, n_frames - f0);
         const size_t n = plane * nf;
@@ -656,6 +689,11 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
             if (cudaMemsetAsync(ws.flags, 0, 2 * sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
             hook_list<<<gn, 256, 0, s>>>(H, W, w, ws.list, cnt, ws.po, ws.best_id, ws.best_rel, ws.flags);
             apply_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.best_rel, ws.po);
+#if BOS_UNWRAP_CHASE
+            // compress the root chains in one launch; no readback: with a crossing edge left
+            // some component always hooks (Borůvka), so the edge count alone ends the loop
+            chase_list<<<gn, 256, 0, s>>>(ws.list, cnt, ws.po);
+#else
             for (int j = 0; j < 64; j += 2) {                             // compress the root chains
                 // two in-place jumps per readback; the flag records only the second, so a pass
                 // that changed nothing ends the compression
@@ -668,6 +706,7 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
                 if (!host_flags[1]) break;
             }
             if (!host_flags[0]) break;                                  // nothing hooked: one tree per frame
+#endif
             {
                 const unsigned gf = (unsigned)std::min<size_t>(((size_t)n_former + 255) / 256, 148 * 16);
                 if (n_former > 0) relink_list<<<gf, 256, 0, s>>>(ws.list0, n_former, ws.po);

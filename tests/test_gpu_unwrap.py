@@ -43,6 +43,23 @@ def test_k_maps_equal_oracle(shape, noise):
     assert np.array_equal(kg, ko), (np.argwhere(kg != ko)[:5], (kg != ko).sum())
 
 
+@pytest.mark.parametrize("shape", [(48, 512), (512, 40)])
+def test_long_component_chains(shape):
+    """Reliability falling monotonically across the frame (φ ∝ s³ along the long axis: the second
+    differences grow with s), so after the tile phase every component's best edge points the
+    same way and the first global round hooks whole rows of tiles into one chain — the case the
+    one-launch chain compression (chase_list) walks longest."""
+    H, W = shape
+    y, x = np.mgrid[0:H, 0:W]
+    s = x if W > H else y
+    truth = 2e-6 * s.astype(np.float64) ** 3 + 0.05 * (y if W > H else x)
+    rng = np.random.default_rng(H + W)
+    w = U.gamma(truth + rng.normal(0, 0.05, (H, W))).astype(np.float32)
+    kg, _ = gpu_k(w)
+    ko = U.unwrap_k(w.astype(np.float64))
+    assert np.array_equal(kg, ko), (np.argwhere(kg != ko)[:5], (kg != ko).sum())
+
+
 def test_smooth_surface_and_in_place_and_stack():
     H, W = 120, 150
     y, x = np.mgrid[0:H, 0:W]
