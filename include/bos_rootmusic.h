@@ -237,13 +237,17 @@ int bos_vertical_profile(const float* phase, int n_frames, int H, int W, float* 
  *   frames_u8   DEVICE [n_frames][H][W] uint8 intensities.  H, W ≥ 2.
  *   fx, fy      carrier in cycles/pixel, |fx|, |fy| ≤ 0.5; the disc must exclude DC
  *               (fx² + fy² > radius²), else BOS_ERR_INVALID_ARG.
- *   out         DEVICE [n_frames][H][W] bos_cf32, written (also the FFT buffer, in place);
- *               must not overlap frames_u8.
- *   d_workspace DEVICE cuFFT work area of ≥ bos_analytic_signal_workspace_bytes(H, W,
- *               n_frames) bytes, caller-owned.
- *   stream      cudaStream_t.  The FFTs use cuFFT (library FFT, plans made and destroyed per
- *               call); the call returns after the work has completed (it synchronises
- *               `stream` before destroying its plans).  Repeated calls should use the planned
+ *   out         DEVICE [n_frames][H][W] bos_cf32, written (the cuFFT path also uses it as
+ *               the FFT buffer, in place); must not overlap frames_u8.
+ *   d_workspace DEVICE work area of ≥ bos_analytic_signal_workspace_bytes(H, W, n_frames)
+ *               bytes, caller-owned: the fused path's spectral-column buffer (8 frames ×
+ *               H·W·8 B at most) or the cuFFT work area.
+ *   stream      cudaStream_t.  Power-of-two H, W ≤ 4096: the fused pruned transform
+ *               (hand-written kernels: rows FFT → the disc's columns only → columns FFT, mask,
+ *               inverse → rows inverse FFT + carrier removal), stream-ordered, no
+ *               synchronisation.  Other sizes: cuFFT (library FFT, plans made and destroyed per
+ *               call); the call then returns after the work has completed (it synchronises
+ *               `stream` before destroying its plans) — repeated calls should use the planned
  *               form below: cuFFT plan creation costs milliseconds to hundreds of ms of host time.
  */
 size_t bos_analytic_signal_workspace_bytes(int H, int W, int n_frames);

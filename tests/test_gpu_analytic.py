@@ -39,11 +39,40 @@ def test_analytic_signal_matches_oracle(shape, remove):
     assert err.max() <= 2e-5 * np.abs(o).max(), (err.max(), np.abs(o).max())
 
 
-def test_planned_analytic_signal_matches_oracle_and_unplanned():
+@pytest.mark.parametrize("remove", [False, True])
+@pytest.mark.parametrize("shape,carrier,radius", [
+    ((9, 256, 512), (synth.CARRIER_FX, synth.CARRIER_FY), 0.05),   # 8-frame chunk + 1
+    ((2, 1024, 1024), (synth.CARRIER_FX, synth.CARRIER_FY), 0.05), # the bench frame size
+    ((3, 64, 2048), (0.47, -0.2), 0.06),                             # carrier near +Nyquist
+    ((2, 4096, 16), (-0.25, 0.4), 0.2),                              # tall, few columns, wide disc
+    ((1, 2, 4), (0.25, -0.5), 0.3),                                  # minimum sizes
+    ((1, 32, 32), (0.2, 0.1), 0.01),                                 # disc between bins: Γ ≡ 0
+])
+def test_fused_path_matches_oracle(shape, carrier, radius, remove):
+    """Power-of-two frames take the fused pruned path (three passes, in-shared-memory FFTs over
+    the kept columns only): element-wise within the same FP32-vs-FP64 bound as the cuFFT path."""
+    T, H, W = shape
+    rng = np.random.default_rng(H * 7 + W)
+    fr = torch.from_numpy(rng.integers(0, 256, (T, H, W), dtype=np.uint8))
+    if H >= 64 and W >= 64:
+        w = synth.workload("C2", H=H, W=W, snr_db=10.0)
+        fr = torch.stack([synth.make_intensity_frame(w, t) for t in range(T)])
+    fx, fy = carrier
+    g = bosrm.bos_analytic_signal(fr.to(DEV), fx, fy, radius, remove)
+    torch.cuda.synchronize()
+    o = A.analytic_signal(fr.numpy(), fx, fy, radius, remove)
+    err = np.abs(g.cpu().numpy().astype(np.complex128) - o)
+    assert err.max() <= 2e-5 * max(np.abs(o).max(), 1e-30) or np.abs(o).max() == 0 and err.max() == 0, \
+        (err.max(), np.abs(o).max())
+
+
+@pytest.mark.parametrize("W", [80, 64])
+def test_planned_analytic_signal_matches_oracle_and_unplanned(W):
     """The caller-owned plan (bos_analytic_plan_*) on a ragged frame count (2 full 8-frame
     batches + 3 single-frame tail FFTs) equals the per-call-plan path bit for bit and the
-    oracle within the FP32 FFT bound; one plan serves calls of different frame counts."""
-    T, H, W = 19, 64, 80
+    oracle within the FP32 FFT bound; one plan serves calls of different frame counts.
+    W = 80: the cuFFT path; W = 64: the fused power-of-two path."""
+    T, H = 19, 64
     w = synth.workload("C2", H=H, W=W, snr_db=10.0)
     fr = torch.stack([synth.make_intensity_frame(w, t) for t in range(T)]).to(DEV)
     plan = bosrm.AnalyticPlan(H, W, T)
