@@ -13,6 +13,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <new>
 
@@ -21,6 +22,9 @@
 namespace {
 
 constexpr int kChunk = 8;   // frames per cuFFT batch / fused-path chunk (bounds the work area)
+#ifndef BOS_F1_SHIFT_CARRIER
+#define BOS_F1_SHIFT_CARRIER 1   // integral carriers removed as a spectral shift (0: always the per-pixel factor)
+#endif
 #ifndef BOS_F1_FUSED
 #define BOS_F1_FUSED 1      // 0: the cuFFT path for every shape (A/B builds)
 #endif
@@ -150,14 +154,15 @@ struct Fft4 {
 };
 // one N-point DFT of S[0..N) (natural order in and out) by the threads t < Fft4::T of its group;
 // every thread of the CTA calls it (barriers inside); the caller synchronises before
+// (rot: the input read cyclically shifted, x'[n] = S[(n + rot) mod N])
 template <int N1, int N2, bool INV>
-__device__ __forceinline__ void fft4(float2* S, const float2* tw, int t) {
+__device__ __forceinline__ void fft4(float2* S, const float2* tw, int t, int rot = 0) {
     using F = Fft4<N1, N2>;
     {
         float2 a[N1];
         if (t < N2) {
 #pragma unroll
-            for (int n1 = 0; n1 < N1; ++n1) a[n1] = S[N2 * n1 + t];
+            for (int n1 = 0; n1 < N1; ++n1) a[n1] = S[(N2 * n1 + t + rot) & (F::N - 1)];
         }
         __syncthreads();
         if (t < N2) {
@@ -223,8 +228,10 @@ __global__ void __launch_bounds__(kFusedThreads) f1_rows_fwd(const uint8_t* __re
 
 // B: CTA = G kept columns of one frame (H = N1·N2): FFT over y, the disc mask × 1/(H·W), inverse
 template <int N1, int N2>
+// sy: spectral shift of the kept bins by −sy rows (an integral carrier f_y·H removed in the
+// frequency domain, see f1_rows_inv), else 0
 __global__ void __launch_bounds__(kFusedThreads) f1_cols(int W, int G, int kx0, int nx, double fx, double fy, double r2,
-                                                         float2* __restrict__ X) {
+                                                         int sy, float2* __restrict__ X) {
     using F = Fft4<N1, N2>;
     constexpr int H = F::N;
     extern __shared__ float2 sm[];
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(kFusedThreads) f1_cols(int W, int G, int kx0, 
         S[a * F::SZ + ky] = v;
     }
     __syncthreads();
-    fft4<N1, N2, true>(Sg, tw, tf);
+    fft4<N1, N2, true>(Sg, tw, tf, sy);
     for (int i = threadIdx.x; i < G * H; i += blockDim.x) {
         const int a = i / H, y = i - a * H;
         if (j0 + a < nx) X[((size_t)f * nx + j0 + a) * H + y] = S[a * F::SZ + y];
@@ -263,10 +270,13 @@ __global__ void __launch_bounds__(kFusedThreads) f1_cols(int W, int G, int kx0, 
 }
 
 // C: CTA = G rows of one frame (W = N1·N2): the kept bins → inverse FFT over x → (carrier
-// removal, e^{−2πi f_x x}·e^{−2πi f_y y} from per-CTA tables, each phase reduced mod 1 in FP64)
+// removal).  remove = 1: e^{−2πi f_x x}·e^{−2πi f_y y} from per-CTA tables, each phase reduced
+// mod 1 in FP64, multiplied into the store; remove = 2 (integral carrier, f_x·W = sx and
+// f_y·H = sy bins): the same factor as a cyclic shift of the spectrum by (−sy, −sx) — exact in
+// the DFT, no per-pixel multiply (rows here, columns in f1_cols)
 template <int N1, int N2>
 __global__ void __launch_bounds__(kFusedThreads) f1_rows_inv(const float2* __restrict__ X, int H, int G, int kx0,
-                                                             int nx, double fx, double fy, int remove,
+                                                             int nx, double fx, double fy, int remove, int sx,
                                                              float2* __restrict__ out) {
     using F = Fft4<N1, N2>;
     constexpr int W = F::N;
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(kFusedThreads) f1_rows_inv(const float2* __res
     const int f = blockIdx.x / per, y0 = (blockIdx.x % per) * G;
     twiddles(tw, W);
     for (int i = threadIdx.x; i < G * F::SZ; i += blockDim.x) S[i] = make_float2(0.0f, 0.0f);
-    if (remove) {
+    if (remove == 1) {
         for (int i = threadIdx.x; i < W + G; i += blockDim.x) {
             double ph = i < W ? fx * (double)i : fy * (double)(y0 + i - W);
             ph -= floor(ph);
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(kFusedThreads) f1_rows_inv(const float2* __res
     __syncthreads();
     for (int i = threadIdx.x; i < G * nx; i += blockDim.x) {
         const int j = i / G, a = i - j * G;
-        S[a * F::SZ + ((kx0 + j) & (W - 1))] = X[((size_t)f * nx + j) * H + y0 + a];
+        S[a * F::SZ + ((kx0 + j - sx) & (W - 1))] = X[((size_t)f * nx + j) * H + y0 + a];
     }
     __syncthreads();
     const int g = threadIdx.x / F::T;
@@ -299,7 +309,7 @@ __global__ void __launch_bounds__(kFusedThreads) f1_rows_inv(const float2* __res
     for (int i = threadIdx.x; i < G * W; i += blockDim.x) {
         const int a = i / W, c = i - a * W;
         float2 v = S[a * F::SZ + c];
-        if (remove) v = f2mul(v, f2mul(ex[c], ex[W + a]));
+        if (remove == 1) v = f2mul(v, f2mul(ex[c], ex[W + a]));
         o[i] = v;
     }
 }
@@ -369,7 +379,7 @@ namespace {
 
 template <int N1, int N2>
 int launch_rows(const uint8_t* in, float2* X, float2* out, int nb, int H, int kx0, int nx, double fx, double fy,
-                int remove, cudaStream_t s, bool fwd) {
+                int remove, int sx, cudaStream_t s, bool fwd) {
     using F = Fft4<N1, N2>;
     if (fwd) {
         const int G = std::max(1, std::min(fused_groups<N1, N2>(), H / 2));
@@ -382,18 +392,18 @@ int launch_rows(const uint8_t* in, float2* X, float2* out, int nb, int H, int kx
         const size_t sm = fused_smem<N1, N2>(G) + (size_t)(F::N + G) * sizeof(float2);
         if (cudaFuncSetAttribute(f1_rows_inv<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
             return BOS_ERR_CUDA;
-        f1_rows_inv<N1, N2><<<(unsigned)(nb * (H / G)), G * F::T, sm, s>>>(X, H, G, kx0, nx, fx, fy, remove, out);
+        f1_rows_inv<N1, N2><<<(unsigned)(nb * (H / G)), G * F::T, sm, s>>>(X, H, G, kx0, nx, fx, fy, remove, sx, out);
     }
     return cudaGetLastError() == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 template <int N1, int N2>
-int launch_cols(float2* X, int nb, int W, int kx0, int nx, double fx, double fy, double r2, cudaStream_t s) {
+int launch_cols(float2* X, int nb, int W, int kx0, int nx, double fx, double fy, double r2, int sy, cudaStream_t s) {
     using F = Fft4<N1, N2>;
     const int G = std::max(1, std::min(fused_groups<N1, N2>(), nx));
     const size_t sm = fused_smem<N1, N2>(G);
     if (cudaFuncSetAttribute(f1_cols<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
         return BOS_ERR_CUDA;
-    f1_cols<N1, N2><<<(unsigned)(nb * ((nx + G - 1) / G)), G * F::T, sm, s>>>(W, G, kx0, nx, fx, fy, r2, X);
+    f1_cols<N1, N2><<<(unsigned)(nb * ((nx + G - 1) / G)), G * F::T, sm, s>>>(W, G, kx0, nx, fx, fy, r2, sy, X);
     return cudaGetLastError() == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 // N = 2^logN → (N1, N2) = (2^⌈logN/2⌉, 2^⌊logN/2⌋)
@@ -409,6 +419,12 @@ int run_fused(bos_analytic_plan* pl, const uint8_t* frames_u8, int n_frames, dou
     if (nx == 0)                                     // no bin inside the disc: Γ ≡ 0
         return cudaMemsetAsync(out, 0, plane * (size_t)n_frames * sizeof(bos_cf32), s) == cudaSuccess ? BOS_OK
                                                                                                   : BOS_ERR_CUDA;
+    // an integral carrier (f_x·W, f_y·H whole bins) is removed as a spectral shift
+    const double cxw = fx * (double)W, cyh = fy * (double)H;
+    const bool integral = remove && BOS_F1_SHIFT_CARRIER && cxw == std::floor(cxw) && cyh == std::floor(cyh);
+    const int rmode = !remove ? 0 : (integral ? 2 : 1);
+    const int sx = integral ? (int)(((long long)cxw % W + W) % W) : 0;
+    const int sy = integral ? (int)(((long long)cyh % H + H) % H) : 0;
     float2* X = static_cast<float2*>(d_workspace);
     for (int f0 = 0; f0 < n_frames; f0 += pl->batch) {
         const int nb = std::min(pl->batch, n_frames - f0);
@@ -416,21 +432,21 @@ int run_fused(bos_analytic_plan* pl, const uint8_t* frames_u8, int n_frames, dou
         float2* o = reinterpret_cast<float2*>(out) + (size_t)f0 * plane;
         int rc = BOS_ERR_UNSUPPORTED;
         switch (logW) {
-#define BOS_F1_ROWS_FWD(L, A, B) case L: rc = launch_rows<A, B>(in, X, o, nb, H, kx0, nx, fx, fy, remove, s, true); break;
+#define BOS_F1_ROWS_FWD(L, A, B) case L: rc = launch_rows<A, B>(in, X, o, nb, H, kx0, nx, fx, fy, rmode, sx, s, true); break;
             BOS_F1_SIZES(BOS_F1_ROWS_FWD)
 #undef BOS_F1_ROWS_FWD
         }
         if (rc != BOS_OK) return rc;
         rc = BOS_ERR_UNSUPPORTED;
         switch (logH) {
-#define BOS_F1_COLS(L, A, B) case L: rc = launch_cols<A, B>(X, nb, W, kx0, nx, fx, fy, radius * radius, s); break;
+#define BOS_F1_COLS(L, A, B) case L: rc = launch_cols<A, B>(X, nb, W, kx0, nx, fx, fy, radius * radius, sy, s); break;
             BOS_F1_SIZES(BOS_F1_COLS)
 #undef BOS_F1_COLS
         }
         if (rc != BOS_OK) return rc;
         rc = BOS_ERR_UNSUPPORTED;
         switch (logW) {
-#define BOS_F1_ROWS_INV(L, A, B) case L: rc = launch_rows<A, B>(in, X, o, nb, H, kx0, nx, fx, fy, remove, s, false); break;
+#define BOS_F1_ROWS_INV(L, A, B) case L: rc = launch_rows<A, B>(in, X, o, nb, H, kx0, nx, fx, fy, rmode, sx, s, false); break;
             BOS_F1_SIZES(BOS_F1_ROWS_INV)
 #undef BOS_F1_ROWS_INV
         }
