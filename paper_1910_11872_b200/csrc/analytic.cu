@@ -96,7 +96,10 @@ __global__ void remove_carrier(float2* __restrict__ g, int T, int H, int W, doub
 // threads run N2-point DFTs over the (padded) rows — two shared-memory round trips per FFT;
 // twiddles W_N^m from sincospif of exact m/N.
 constexpr int kFusedMaxN = 4096;
-constexpr int kFusedThreads = 256;
+#ifndef BOS_F1_THREADS
+#define BOS_F1_THREADS 128   // measured per 100 1024² frames: 64 → 1.065, 128 → 1.055, 256 → 1.119, 512 → 1.366 ms
+#endif
+constexpr int kFusedThreads = BOS_F1_THREADS;   // threads per CTA (= FFT groups × threads per FFT)
 
 __device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
