@@ -28,11 +28,26 @@ namespace {
 
 __device__ __forceinline__ double fin(float v) { return isfinite(v) ? (double)v : 0.0; }
 
-// γ(d) = d − 2π·ceil((d − π)/2π), same operation order as oracle.unwrap.gamma
+// γ(d) = d − 2π·ceil((d − π)/2π), same operation order as oracle.unwrap.gamma.  Only ceil of
+// the quotient enters the result, so the correctly rounded division is needed only where the
+// product by 1/2π (within 2 ulp of x/2π, same sign) lies within a few ulp of a nonzero integer;
+// elsewhere both quotients have the same ceiling (the FP64 divide was 8 of the reliability
+// kernel's 9 divisions)
+#ifndef BOS_UNWRAP_FAST_GAMMA
+#define BOS_UNWRAP_FAST_GAMMA 1
+#endif
 __device__ __forceinline__ double gam(double d) {
     const double two_pi = 6.283185307179586;   // 2.0 * np.pi
     const double pi = 3.141592653589793;
-    const double c = ceil(__ddiv_rn(__dsub_rn(d, pi), two_pi));
+    const double x = __dsub_rn(d, pi);
+    double c;
+    if (BOS_UNWRAP_FAST_GAMMA) {
+        const double q = __dmul_rn(x, 0.15915494309189535);          // fl(1/2π)
+        const double n = rint(q);
+        c = (n != 0.0 && fabs(q - n) <= 1e-14 * fabs(q)) ? ceil(__ddiv_rn(x, two_pi)) : ceil(q);
+    } else {
+        c = ceil(__ddiv_rn(x, two_pi));
+    }
     return __dsub_rn(d, __dmul_rn(two_pi, c));
 }
 
