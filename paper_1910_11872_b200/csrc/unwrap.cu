@@ -92,18 +92,12 @@ __device__ __forceinline__ unsigned long long find2(const unsigned long long* po
 
 
 // edge id e = 2p (p → p+1) or 2p+1 (p → p+W), p = frame·H·W + y·W + x (a batch of frames is one
-// forest of independent grids); returns false for the missing border edges
-__device__ __forceinline__ bool edge_ends(unsigned e, int H, int W, int& p, int& q) {
+// forest of independent grids).  Every id these kernels see comes from the tile phase's
+// crossing-edge lists (or their compactions, or a root's best edge from them), which hold only
+// existing edges — so no border test, and no integer divisions, are needed here
+__device__ __forceinline__ bool edge_ends(unsigned e, int /*H*/, int W, int& p, int& q) {
     p = (int)(e >> 1);
-    const int loc = p % (H * W);
-    const int x = loc % W, y = loc / W;
-    if (e & 1u) {
-        if (y + 1 >= H) return false;
-        q = p + W;
-    } else {
-        if (x + 1 >= W) return false;
-        q = p + 1;
-    }
+    q = (e & 1u) ? p + W : p + 1;
     return true;
 }
 
