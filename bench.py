@@ -473,7 +473,7 @@ def run_cuda(args, world, rank, local):
 
     # e2e: the same step through the C-ABI host-buffer entry point (H2D/D2H in the region)
     e2e = None
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5 if not c5 else 1))
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 10 if not c5 else 1))
     if e2e_steps > 0:
         h_frames = frames.cpu().pin_memory()
         h_out = torch.empty(T, H, W, dtype=torch.float32).pin_memory()
@@ -499,7 +499,7 @@ def run_cuda(args, world, rank, local):
         torch.cuda.synchronize()
         e_ms = sharding.max_over_ranks(a.elapsed_time(b), dev)
         e2e = {"value": out_frames * plane * e2e_steps / (e_ms / 1e3) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": (T + 1) * plane * 8, "d2h_bytes_per_step": T * plane * 5,
+               "h2d_bytes_per_step": T * plane * 8, "d2h_bytes_per_step": T * plane * 5,
                "steps": e2e_steps, "chunk_frames": args.chunk_frames,
                "api": "bos_rootmusic_demod_stack_host (pinned host buffers)"}
         # consistency: the host path produced the device path's bytes
