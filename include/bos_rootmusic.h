@@ -110,6 +110,11 @@ int bos_rootmusic_demod(const bos_cf32* frames, int n_frames, int H, int W,
  *   out[t] ← wrap(α_t − ref_phase_out) for every t ≠ ref_index (one launch per side of it);
  *   out[ref_index] ← ref_phase_out − ref_phase_out: exactly 0, NaN where α_ref is — what
  *   demodulating the reference frame against itself would give, without doing it twice.
+ *   Stacks of ≤ 2^20 pixels in all (a 512² reference + flow pair, …) instead run every frame
+ *   raw in ONE launch (a one-frame launch leaves most of its last wave idle), copy the
+ *   reference's α to ref_phase_out and form wrap(α_t − α_ref) by a pointwise kernel with the
+ *   fused store's FP32 operations — the same outputs (an α of exactly −π, which the raw store
+ *   wraps to +π, is the one case that can differ by rounding).
  *   ref_index      0 ≤ ref_index < n_frames.
  *   ref_phase_out  DEVICE [H][W] float32, written (caller-owned scratch / result); must not
  *                  overlap frames or out_phase.

@@ -194,6 +194,11 @@ int demod_impl(const bos_cf32* frames, int n_frames, int H, int W, int window_le
     return e == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
 }
 
+#ifndef BOS_SMALL_STACK_PX
+#define BOS_SMALL_STACK_PX (1u << 20)   // ≤ this many pixels in the whole stack: one raw launch + difference
+#endif
+constexpr size_t kSmallStackPx = BOS_SMALL_STACK_PX;
+
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // per-device pipeline objects of bos_rootmusic_demod_stack_host (created on first use, kept
@@ -212,6 +217,19 @@ std::mutex g_pipe_mutex[kPipeDevices];
 __global__ void self_difference_kernel(const float* __restrict__ a, size_t n, float* __restrict__ out) {
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = a[i] - a[i];
+}
+
+// out[i] = wrap(out[i] − ref[i mod plane]) in place: the fused store's reference difference
+// (demod_kernel.cuh a7, same FP32 operations) for the small-stack path of
+// bos_rootmusic_demod_stack
+__global__ void ref_difference_kernel(float* __restrict__ out, size_t n, size_t plane, const float* __restrict__ ref) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float a = out[i] - ref[i % plane];
+        if (a > CUDART_PI_F) a -= 2.0f * CUDART_PI_F;
+        if (a <= -CUDART_PI_F) a += 2.0f * CUDART_PI_F;
+        out[i] = a;
+    }
 }
 
 // Eq.(17): ∂n/∂x = (1/(2 μ f_x)) (n0/L²) φ — a pointwise scale (vectorised, HBM-bound).
@@ -341,6 +359,22 @@ int bos_rootmusic_demod_stack(const bos_cf32* frames, int n_frames, int H, int W
     if (out_phase == nullptr || !is_device_ptr(out_phase)) return BOS_ERR_INVALID_ARG;
     if (overlaps(ref_phase_out, plane * sizeof(float), out_phase, plane * (size_t)n_frames * sizeof(float)))
         return BOS_ERR_INVALID_ARG;
+    cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+    // small stacks (a reference + flow pair of 512² frames, …): every frame raw in ONE launch,
+    // then the reference difference by a pointwise kernel — a one-frame launch leaves most of
+    // the last wave of the GPU idle, and the flow launch could not start before it ended
+    if (n_frames > 1 && plane * (size_t)n_frames <= kSmallStackPx) {
+        rc = demod_impl(frames, n_frames, H, W, window_len, model_order, nullptr, out_phase, flags, nullptr, stream,
+                        true);
+        if (rc != BOS_OK) return rc;
+        if (cudaMemcpyAsync(ref_phase_out, out_phase + (size_t)ref_index * plane, plane * sizeof(float),
+                            cudaMemcpyDeviceToDevice, s0) != cudaSuccess)
+            return BOS_ERR_CUDA;
+        const size_t n = plane * (size_t)n_frames;
+        const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 8);
+        ref_difference_kernel<<<blocks, 256, 0, s0>>>(out_phase, n, plane, ref_phase_out);
+        return cudaGetLastError() == cudaSuccess ? BOS_OK : BOS_ERR_CUDA;
+    }
     // the reference frame once (raw α, and its flags); its own output wrap(α_ref − α_ref) is
     // exactly 0 (NaN where α_ref is) — written by a pointwise kernel instead of demodulating
     // the frame a second time; the other frames in ≤ 2 launches around it
