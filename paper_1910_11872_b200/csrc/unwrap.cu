@@ -101,41 +101,34 @@ __device__ __forceinline__ bool edge_ends(unsigned e, int /*H*/, int W, int& p, 
     return true;
 }
 
-// pass 1: every component's largest incident cross-edge reliability (positive doubles order as u64)
-__device__ __forceinline__ void edge_max_one(unsigned e, int H, int W, const double* __restrict__ rel,
-                                             const unsigned long long* __restrict__ po, unsigned long long* best_rel) {
-    int p, q;
-    if (!edge_ends(e, H, W, p, q)) return;
-    const int rp = par(find2(po, p)), rq = par(find2(po, q));
-    if (rp == rq) return;
-    const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
-    atomicMax(best_rel + rp, key);
-    atomicMax(best_rel + rq, key);
-}
-// pass 2: among the edges at that reliability, the smallest id
-__device__ __forceinline__ void edge_argmin_one(unsigned e, int H, int W, const double* __restrict__ rel,
-                                                const unsigned long long* __restrict__ po,
-                                                const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
-    int p, q;
-    if (!edge_ends(e, H, W, p, q)) return;
-    const int rp = par(find2(po, p)), rq = par(find2(po, q));
-    if (rp == rq) return;
-    const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
-    if (key == best_rel[rp]) atomicMin(best_id + rp, e);
-    if (key == best_rel[rq]) atomicMin(best_id + rq, e);
-}
-// the global rounds: only the edges that still cross components (the compacted list)
+// the global rounds: only the edges that still cross components (the compacted list).  Pass 1
+// also stores each edge's (root p, root q, key) in rec[k], so pass 2 reads them sequentially
+// instead of repeating the two-hop root lookups and reliability loads (nothing changes the
+// roots between the two passes)
 __global__ void edge_max_list(const unsigned* __restrict__ list, unsigned n, int H, int W,
                               const double* __restrict__ rel, const unsigned long long* __restrict__ po,
-                              unsigned long long* best_rel) {
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-        edge_max_one(list[k], H, W, rel, po, best_rel);
+                              unsigned long long* best_rel, uint4* __restrict__ rec) {
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        int p, q;
+        edge_ends(list[k], H, W, p, q);
+        const int rp = par(find2(po, p)), rq = par(find2(po, q));
+        const unsigned long long key = (unsigned long long)__double_as_longlong(__dadd_rn(rel[p], rel[q]));
+        rec[k] = make_uint4((unsigned)rp, (unsigned)rq, (unsigned)key, (unsigned)(key >> 32));
+        if (rp == rq) continue;
+        atomicMax(best_rel + rp, key);
+        atomicMax(best_rel + rq, key);
+    }
 }
-__global__ void edge_argmin_list(const unsigned* __restrict__ list, unsigned n, int H, int W,
-                                 const double* __restrict__ rel, const unsigned long long* __restrict__ po,
+__global__ void edge_argmin_list(const unsigned* __restrict__ list, unsigned n, const uint4* __restrict__ rec,
                                  const unsigned long long* __restrict__ best_rel, unsigned* best_id) {
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-        edge_argmin_one(list[k], H, W, rel, po, best_rel, best_id);
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint4 r = rec[k];
+        if (r.x == r.y) continue;
+        const unsigned long long key = (unsigned long long)r.z | ((unsigned long long)r.w << 32);
+        const unsigned e = list[k];
+        if (key == best_rel[r.x]) atomicMin(best_id + r.x, e);
+        if (key == best_rel[r.y]) atomicMin(best_id + r.y, e);
+    }
 }
 
 // ---- crossing-edge compaction: after a round's re-link every node points at its final root,
@@ -577,6 +570,7 @@ struct Ws {
     unsigned *edges, *edges2;    // crossing-edge lists (ping-pong), ≤ 2n ids each
     uint8_t* ebits;              // filter flags, one byte per 8 edges
     unsigned *bcount, *boff;     // filter per-block counts / offsets
+    uint4* rec;                  // per listed edge: (root p, root q, key) from pass 1 for pass 2
 };
 
 size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
@@ -602,7 +596,9 @@ size_t ws_layout(size_t n, int F, char* base, Ws* ws) {
     char* eb = take(nblk * kFiltThreads);
     char* bc = take(nblk * sizeof(unsigned));
     char* bo = take(nblk * sizeof(unsigned));
+    char* rc = take(2 * n * sizeof(uint4));
     if (ws) {
+        ws->rec = (uint4*)rc;
         ws->rel = (double*)r;
         ws->po = (unsigned long long*)p1;
         ws->list = (unsigned*)l1;
@@ -692,8 +688,8 @@ int bos_unwrap(const float* wrapped, int n_frames, int H, int W, float* unwrappe
             if (n_edges == 0) break;                                    // no crossing edge: done
             {
                 const unsigned gl = (unsigned)std::min<size_t>(((size_t)n_edges + 255) / 256, 148 * 16);
-                edge_max_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel);
-                edge_argmin_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel, ws.best_id);
+                edge_max_list<<<gl, 256, 0, s>>>(E, n_edges, H, W, ws.rel, ws.po, ws.best_rel, ws.rec);
+                edge_argmin_list<<<gl, 256, 0, s>>>(E, n_edges, ws.rec, ws.best_rel, ws.best_id);
             }
             if (cudaMemsetAsync(ws.flags, 0, 2 * sizeof(int), s) != cudaSuccess) return BOS_ERR_CUDA;
             hook_list<<<gn, 256, 0, s>>>(H, W, w, ws.list, cnt, ws.po, ws.best_id, ws.best_rel, ws.flags);

@@ -149,9 +149,9 @@ def test_unwrap_workspace_and_errors(L):
     n = 100 * 64
     al = lambda v: (v + 255) // 256 * 256  # noqa: E731
 
-    def edges(n):       # two crossing-edge lists (2n ids), filter flag bytes, per-block counts/offsets
-        nb = (2 * n + 2047) // 2048
-        return 2 * al(4 * 2 * n) + al(nb * 256) + 2 * al(4 * nb)
+    def edges(n):       # two crossing-edge lists (2n ids), filter flag bytes, per-block counts/offsets,
+        nb = (2 * n + 2047) // 2048     # and the per-edge (root, root, key) records of the edge passes
+        return 2 * al(4 * 2 * n) + al(nb * 256) + 2 * al(4 * nb) + al(16 * 2 * n)
     expect = al(8 * n) + 5 * al(4 * n) + al(8 * n) + al(4 * n) + al(16) + al(8) + al(4) + edges(n)
     assert L.bos_unwrap_workspace_bytes(100, 64, 1) == expect
     n3 = 3 * n
