@@ -179,6 +179,22 @@ def test_host_api_matches_device_api():
     assert torch.equal(h_out2, dev_out.cpu())
 
 
+@pytest.mark.parametrize("T", [1, 2])
+def test_host_and_device_stack_tiny(T):
+    """One- and two-frame stacks: the host pipeline (the reference chunk alone, then at most one
+    flow chunk) and the device stack (one-frame path / small-stack raw launch + difference)
+    give the same bytes; the reference's own output is exactly 0."""
+    w = synth.workload("C3", H=48, W=40)
+    stack = synth.make_stack(w, frames=range(T), snr_db=10.0)
+    d_out, d_fl, d_ref = bosrm.bos_rootmusic_demod_stack(stack.to(DEV), 8, ref_index=T - 1, flags=True)
+    h_out, h_fl = bosrm.bos_rootmusic_demod_stack_host(stack.pin_memory(), 8, ref_index=T - 1, h_flags=True,
+                                                      chunk_frames=1)
+    torch.cuda.synchronize()
+    assert torch.equal(h_out, d_out.cpu()) and torch.equal(h_fl, d_fl.cpu())
+    r = d_out[T - 1]
+    assert torch.all(r[torch.isfinite(r)] == 0)
+
+
 @pytest.mark.parametrize("ref_index,chunk,M", [(3, 4, 8), (9, 5, 8), (6, 3, 15), (0, 16, 5)])
 def test_host_api_ramped_chunks(ref_index, chunk, M):
     """The host pipeline's chunk schedule (the reference frame alone first; the other frames in
