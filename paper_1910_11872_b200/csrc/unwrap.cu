@@ -292,13 +292,20 @@ __global__ void __launch_bounds__(kTile * kTile, BOS_UNWRAP_TILE_MIN_BLOCKS) til
         bkey[l] = 0ull;
         bid[l] = 0xffffffffu;
         __syncthreads();
+        // the incident edges that still leave the component; an edge that became internal stays
+        // internal, so it leaves `has` for good
+        unsigned cross = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (((has >> k) & 1u) && (ol(k) < 0 || tpar(node[ol(k)]) != r)) atomicMax(bkey + r, skey[k][l]);
+            if (((has >> k) & 1u) && (ol(k) < 0 || tpar(node[ol(k)]) != r)) cross |= 1u << k;
+        has = cross;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if ((cross >> k) & 1u) atomicMax(bkey + r, skey[k][l]);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (((has >> k) & 1u) && (ol(k) < 0 || tpar(node[ol(k)]) != r) && skey[k][l] == bkey[r]) atomicMin(bid + r, eid(k));
+            if (((cross >> k) & 1u) && skey[k][l] == bkey[r]) atomicMin(bid + r, eid(k));
         __syncthreads();
         // roots hook across their best edge when it stays inside the tile; the edge's tile-side
         // end that belongs to this component is p_in, the other end q_out
