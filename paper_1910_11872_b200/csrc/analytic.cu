@@ -392,7 +392,7 @@ int launch_rows(const uint8_t* in, float2* X, float2* out, int nb, int H, int kx
         f1_rows_fwd<N1, N2><<<(unsigned)(nb * (H / (2 * G))), G * F::T, sm, s>>>(in, H, G, kx0, nx, X);
     } else {
         const int G = std::max(1, std::min(fused_groups<N1, N2>(), H));
-        const size_t sm = fused_smem<N1, N2>(G) + (size_t)(F::N + G) * sizeof(float2);
+        const size_t sm = fused_smem<N1, N2>(G) + (remove == 1 ? (size_t)(F::N + G) * sizeof(float2) : 0);   // carrier tables only for the per-pixel factor
         if (cudaFuncSetAttribute(f1_rows_inv<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
             return BOS_ERR_CUDA;
         f1_rows_inv<N1, N2><<<(unsigned)(nb * (H / G)), G * F::T, sm, s>>>(X, H, G, kx0, nx, fx, fy, remove, sx, out);
