@@ -99,7 +99,12 @@ constexpr int kFusedMaxN = 4096;
 #ifndef BOS_F1_THREADS
 #define BOS_F1_THREADS 128   // measured per 100 1024² frames: 64 → 1.065, 128 → 1.055, 256 → 1.119, 512 → 1.366 ms
 #endif
-constexpr int kFusedThreads = BOS_F1_THREADS;   // threads per CTA (= FFT groups × threads per FFT)
+constexpr int kFusedThreads = BOS_F1_THREADS;
+#ifndef BOS_F1_MIN_BLOCKS
+#define BOS_F1_MIN_BLOCKS 6     // CTAs/SM the register budget targets for FFTs of ≤ 1024 points (80 registers, no spills)
+#endif
+template <int N1, int N2>
+constexpr int f1_min_blocks() { return N1 * N2 <= 1024 ? BOS_F1_MIN_BLOCKS : 1; }   // threads per CTA (= FFT groups × threads per FFT)
 
 __device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
@@ -200,7 +205,7 @@ constexpr int fused_groups() { return kFusedThreads / Fft4<N1, N2>::T; }
 
 // A: CTA = G packed row pairs of one frame (W = N1·N2); out X[f][j][y], kx = (kx0 + j) mod W
 template <int N1, int N2>
-__global__ void __launch_bounds__(kFusedThreads) f1_rows_fwd(const uint8_t* __restrict__ in, int H, int G, int kx0,
+__global__ void __launch_bounds__(kFusedThreads, f1_min_blocks<N1, N2>()) f1_rows_fwd(const uint8_t* __restrict__ in, int H, int G, int kx0,
                                                              int nx, float2* __restrict__ X) {
     using F = Fft4<N1, N2>;
     constexpr int W = F::N;
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kFusedThreads) f1_rows_fwd(const uint8_t* __re
 template <int N1, int N2>
 // sy: spectral shift of the kept bins by −sy rows (an integral carrier f_y·H removed in the
 // frequency domain, see f1_rows_inv), else 0
-__global__ void __launch_bounds__(kFusedThreads) f1_cols(int W, int G, int kx0, int nx, double fx, double fy, double r2,
+__global__ void __launch_bounds__(kFusedThreads, f1_min_blocks<N1, N2>()) f1_cols(int W, int G, int kx0, int nx, double fx, double fy, double r2,
                                                          int sy, float2* __restrict__ X) {
     using F = Fft4<N1, N2>;
     constexpr int H = F::N;
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(kFusedThreads) f1_cols(int W, int G, int kx0, 
 // f_y·H = sy bins): the same factor as a cyclic shift of the spectrum by (−sy, −sx) — exact in
 // the DFT, no per-pixel multiply (rows here, columns in f1_cols)
 template <int N1, int N2>
-__global__ void __launch_bounds__(kFusedThreads) f1_rows_inv(const float2* __restrict__ X, int H, int G, int kx0,
+__global__ void __launch_bounds__(kFusedThreads, f1_min_blocks<N1, N2>()) f1_rows_inv(const float2* __restrict__ X, int H, int G, int kx0,
                                                              int nx, double fx, double fy, int remove, int sx,
                                                              float2* __restrict__ out) {
     using F = Fft4<N1, N2>;
